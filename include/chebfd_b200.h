@@ -1,0 +1,262 @@
+/* chebfd_b200 -- B200-native ChebFD hot path behind a plain C ABI.
+ *
+ * This is the drop-in boundary.  The reference has no FFI; its
+ * boundary is the C++ template API in /root/reference/proj/include/chebfd/*.hpp
+ * instantiated for double and std::complex<double>.  Each entry point below
+ * names the reference function it replaces (file:line relative to
+ * /root/reference/proj).  include/chebfd_b200.hpp restores the reference's
+ * C++ signatures and exception types on top of this header.
+ *
+ * Conventions
+ *  - Every function returns int status: CHEBFD_OK (0) or a code naming the
+ *    reference exception type; chebfd_last_error() returns the message
+ *    (thread-local).
+ *  - kind: CHEBFD_REAL64 = double, CHEBFD_COMPLEX128 = std::complex<double>
+ *    (interleaved re,im), scalar.hpp:12.
+ *  - Block vectors are D x nb ROW-MAJOR (entry (i,k) at i*nb+k), exactly the
+ *    reference contract block_vector.hpp:15-16, on the device.
+ *  - Host buffers are plain pointers; nothing in this header uses torch types.
+ *  - A context drives one GPU on one stream.  Not thread-safe per context.
+ *    A distributed context (chebfd_ctx_create_dist) row-partitions matrices
+ *    and blocks across ranks (one process per GPU) and exchanges halos and
+ *    reductions with NCCL.
+ */
+#ifndef CHEBFD_B200_H
+#define CHEBFD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: map to the reference's exception types ---------------- */
+enum {
+    CHEBFD_OK = 0,
+    CHEBFD_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument: shape, alias, degree */
+    CHEBFD_ERR_RUNTIME = 2,          /* std::runtime_error: numerical failure */
+    CHEBFD_ERR_DOMAIN = 3,           /* std::domain_error */
+    CHEBFD_ERR_OUT_OF_RANGE = 4,     /* std::out_of_range */
+    CHEBFD_ERR_CUDA = 5,             /* CUDA runtime / cuBLAS / cuSOLVER failure */
+    CHEBFD_ERR_NCCL = 6,             /* NCCL failure */
+    CHEBFD_ERR_UNSUPPORTED = 7
+};
+
+enum { CHEBFD_REAL64 = 0, CHEBFD_COMPLEX128 = 1 };                     /* scalar.hpp:12 */
+enum { CHEBFD_PERIODIC_XY_OPEN_Z = 0, CHEBFD_PERIODIC_ALL = 1, CHEBFD_OPEN_ALL = 2 }; /* models.hpp:13 */
+enum { CHEBFD_KERNEL_NONE = 0, CHEBFD_KERNEL_FEJER = 1, CHEBFD_KERNEL_JACKSON = 2,
+       CHEBFD_KERNEL_LANCZOS = 3 };                                     /* filter.hpp:12 */
+
+typedef struct chebfd_ctx chebfd_ctx;
+typedef struct chebfd_matrix chebfd_matrix;
+typedef struct chebfd_block chebfd_block;
+
+/* Message of the last failing call on this thread. */
+const char* chebfd_last_error(void);
+/* Library version string. */
+const char* chebfd_version(void);
+
+/* ---- context --------------------------------------------------------------- */
+/* Single-GPU context on `device` (replaces the OpenMP runtime, parallel.hpp:18-54). */
+int chebfd_ctx_create(int device, chebfd_ctx** out);
+/* Distributed context: this process is `rank` of `nranks`, one GPU each; the
+ * 128-byte NCCL unique id comes from chebfd_nccl_unique_id() on rank 0 and is
+ * broadcast by the caller (torch.distributed or MPI). */
+int chebfd_nccl_unique_id(unsigned char id[128]);
+int chebfd_ctx_create_dist(int device, int rank, int nranks, const unsigned char id[128],
+                           chebfd_ctx** out);
+int chebfd_ctx_destroy(chebfd_ctx* ctx);
+int chebfd_ctx_synchronize(chebfd_ctx* ctx);
+/* cudaStream_t the context launches on (for CUDA-event timing by callers). */
+int chebfd_ctx_stream(chebfd_ctx* ctx, void** stream);
+int chebfd_ctx_info(chebfd_ctx* ctx, int* device, int* rank, int* nranks, int* num_sms);
+/* Number of kernels this library launched on ctx since creation (graph
+ * replays count every captured kernel). */
+int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count);
+/* Options: CHEBFD_OPT_GRAPHS (1 = capture apply_filter into cached CUDA
+ * graphs, default 1); CHEBFD_OPT_OVERLAP (1 = overlap the halo exchange with
+ * interior rows, default 1). */
+enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2 };
+int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
+
+/* CUDA-event timing on the context stream: 16 event slots per context. */
+int chebfd_ctx_event_record(chebfd_ctx* ctx, int slot);
+/* Milliseconds between two recorded slots (synchronises on slot b). */
+int chebfd_ctx_event_elapsed(chebfd_ctx* ctx, int slot_a, int slot_b, float* ms);
+
+/* Pinned host memory for end-to-end transfers. */
+int chebfd_host_alloc(size_t bytes, void** out);
+int chebfd_host_free(void* p);
+
+/* ---- lattice models (models.hpp:19-29, models.cpp) ------------------------- */
+typedef struct {
+    int64_t lx, ly, lz; /* lattice size; graphene ignores lz */
+    double t;           /* hopping amplitude */
+    double disorder;    /* V: box disorder on [-V/2, V/2] (full width) */
+    int boundary;       /* CHEBFD_PERIODIC_XY_OPEN_Z etc. */
+    uint64_t seed;      /* mt19937_64 seed for the site potentials */
+} chebfd_lattice;
+
+/* Host CSR of rows [row_begin, row_end) of the graphene / topological
+ * insulator Hamiltonian, bit-identical to graphene() (models.cpp:142-178) /
+ * topological_insulator() (models.cpp:80-140) built by the reference's
+ * Builder (sparse_matrix.hpp:57-84), but generated stencil-direct (no
+ * std::map).  Two-call pattern: with offs == NULL only *nnz (and *dim) are
+ * returned; then pass arrays of (row_end-row_begin)+1 / nnz / nnz (values
+ * double or interleaved complex).  offs are relative to row_begin. */
+int chebfd_csr_graphene(const chebfd_lattice* spec, int64_t row_begin, int64_t row_end,
+                        int64_t* dim, int64_t* nnz, int64_t* offs, int64_t* cols, void* vals);
+int chebfd_csr_topological_insulator(const chebfd_lattice* spec, int64_t row_begin,
+                                     int64_t row_end, int64_t* dim, int64_t* nnz, int64_t* offs,
+                                     int64_t* cols, void* vals);
+
+/* ---- device sparse matrix (SELL-C-sigma, C = 32, sigma = 1) ----------------- */
+/* From a full host CSR (SparseMatrix ctor + validate, sparse_matrix.hpp:22-100).
+ * In a distributed context every rank passes the full matrix and keeps its
+ * row partition. */
+int chebfd_matrix_from_csr(chebfd_ctx* ctx, int kind, int64_t dim, const int64_t* row_offsets,
+                           const int64_t* col_indices, const void* values, chebfd_matrix** out);
+/* Stencil-direct device matrices of the two lattice models.  In a
+ * distributed context each rank generates only its rows, partitioned on
+ * lattice planes (TI z-planes, graphene y-rows). */
+int chebfd_matrix_graphene(chebfd_ctx* ctx, const chebfd_lattice* spec, chebfd_matrix** out);
+int chebfd_matrix_topological_insulator(chebfd_ctx* ctx, const chebfd_lattice* spec,
+                                        chebfd_matrix** out);
+int chebfd_matrix_destroy(chebfd_matrix* a);
+typedef struct {
+    int kind;
+    int64_t dim;          /* global dimension D */
+    int64_t nnz;          /* global nonzeros (reference count, padding excluded) */
+    int64_t local_rows;   /* rows owned by this rank */
+    int64_t row_begin;    /* first global row owned */
+    int64_t local_nnz;    /* nonzeros in owned rows */
+    int64_t sell_entries; /* stored SELL slots incl. padding */
+    int64_t halo_lo, halo_hi; /* halo rows received from the lower / upper neighbour */
+    int chunk;            /* SELL chunk height C */
+    int max_row_len;
+} chebfd_matrix_info;
+int chebfd_matrix_get_info(const chebfd_matrix* a, chebfd_matrix_info* out);
+
+/* ---- block vectors (block_vector.hpp:17-102) -------------------------------- */
+/* A block conforming to matrix `a` (owned rows of this rank), width nb, zero-filled. */
+int chebfd_block_create(chebfd_matrix* a, int64_t width, chebfd_block** out);
+/* A free-standing block of `dim` rows (single-GPU contexts). */
+int chebfd_block_create_dim(chebfd_ctx* ctx, int kind, int64_t dim, int64_t width,
+                            chebfd_block** out);
+int chebfd_block_destroy(chebfd_block* b);
+int chebfd_block_info(const chebfd_block* b, int* kind, int64_t* rows, int64_t* width,
+                      int64_t* row_begin);
+int chebfd_block_upload(chebfd_block* b, const void* host_rowmajor);
+int chebfd_block_download(const chebfd_block* b, void* host_rowmajor);
+int chebfd_block_copy(chebfd_block* dst, const chebfd_block* src);
+int chebfd_block_zero(chebfd_block* b);
+/* BlockVector::randomize (block_vector.hpp:42-51): the same mt19937_64 +
+ * libstdc++ normal_distribution stream over the GLOBAL D x nb block, so a
+ * distributed block equals the reference's rows. Host-generated, uploaded. */
+int chebfd_block_randomize(chebfd_block* b, uint64_t seed);
+/* Device Gaussian fill (Philox counter RNG) -- fast synthetic inputs for
+ * benchmarks; NOT the reference's stream. */
+int chebfd_block_randomize_device(chebfd_block* b, uint64_t seed);
+/* x(:,k) *= s[k] for k < width (used to normalise columns). */
+int chebfd_block_scale_columns(chebfd_block* b, const double* s);
+/* dst(:, d0:d0+n) = src(:, s0:s0+n) */
+int chebfd_block_copy_columns(chebfd_block* dst, int64_t d0, const chebfd_block* src, int64_t s0,
+                              int64_t n);
+int chebfd_block_device_ptr(chebfd_block* b, void** ptr);
+
+/* ---- kernels (kernels.hpp) ---------------------------------------------------- */
+/* Y = (alpha A + beta I) X                                  kernels.hpp:45-69 */
+int chebfd_spmmvm(chebfd_matrix* a, chebfd_block* x, chebfd_block* y, double alpha, double beta);
+/* W <- 2(alpha A + beta I) U - W;  X <- X + coeff W;  optional dots_k =
+ * <x_k(before), w_k(after)> into host `dots` (S[nb]) or NULL.  kernels.hpp:71-118 */
+int chebfd_spmmvm_fused(chebfd_matrix* a, chebfd_block* u, chebfd_block* w, chebfd_block* x,
+                        double alpha, double beta, double coeff, void* dots);
+/* W <- 2(alpha A + beta I) U - W                              kernels.hpp:120-145 */
+int chebfd_recurrence_step(chebfd_matrix* a, chebfd_block* u, chebfd_block* w, double alpha,
+                           double beta);
+/* X <- c0 X + c1 U + c2 W                                     kernels.hpp:147-162 */
+int chebfd_block_axpy_scal(chebfd_block* x, const chebfd_block* u, const chebfd_block* w,
+                           double c0, double c1, double c2);
+/* d_k = <x_k, y_k> -> host S[nb]                               kernels.hpp:194-213 */
+int chebfd_column_dots(const chebfd_block* x, const chebfd_block* y, void* out);
+/* ||x_k|| -> host double[nb]                                    kernels.hpp:234-240 */
+int chebfd_column_norms(const chebfd_block* x, double* out);
+/* G(k,l) = <x_k, y_l> -> host row-major S[nx*ny]               kernels.hpp:164-192 */
+int chebfd_gram(const chebfd_block* x, const chebfd_block* y, void* out);
+/* Y = X B, B host row-major S[nb x bcols], Y width bcols         kernels.hpp:215-232 */
+int chebfd_block_mult_small(const chebfd_block* x, const void* b, int64_t bcols, chebfd_block* y);
+
+/* ---- filter (filter.hpp, filter.cpp) ----------------------------------------- */
+int chebfd_window_coeffs(double target_lo, double target_hi, double bounds_lo, double bounds_hi,
+                         int degree, double* out);                    /* filter.cpp:43-56 */
+int chebfd_kernel_coeffs(int kernel, int mu, int degree, double* out); /* filter.cpp:58-84 */
+/* combined[0..degree] = g_n c_n, alpha = 2/(b-a), beta = (a+b)/(a-b)   filter.cpp:86-99 */
+int chebfd_make_filter(double target_lo, double target_hi, double bounds_lo, double bounds_hi,
+                       int degree, int kernel, int mu, double* combined, double* alpha,
+                       double* beta);
+int chebfd_eval_scalar(const double* combined, int degree, double alpha, double beta,
+                       double bounds_lo, double bounds_hi, double x, double* out); /* :101-114 */
+/* X <- p[A] X in exactly degree*nb column spMVMs (filter.hpp:73-116).  If
+ * moments != NULL it receives m(n,k) = Re<x0_k, T_n(h) x0_k>, (degree+1) x nb
+ * row-major (MomentTable, filter.hpp:61-68). */
+int chebfd_apply_filter(chebfd_matrix* a, chebfd_block* x, const double* combined, int degree,
+                        double alpha, double beta, double* moments);
+/* Same, end to end from a HOST block (row-major, owned rows): H2D, filter, D2H. */
+int chebfd_apply_filter_host(chebfd_matrix* a, void* x_host, int64_t width,
+                             const double* combined, int degree, double alpha, double beta,
+                             double* moments);
+
+/* ---- solver (solver.hpp / solver.cpp) ------------------------------------------- */
+/* SVQB (solver.cpp:32-61): q receives the rank orthonormal columns first. */
+int chebfd_svqb(chebfd_block* y, double drop_tol, chebfd_block* q, int64_t* rank);
+/* Rayleigh-Ritz (solver.cpp:63-91): v = Ritz vectors; values ascending. */
+int chebfd_rayleigh_ritz(chebfd_matrix* a, chebfd_block* q, chebfd_block* v, double* values,
+                         double* residual_norms);
+
+/* ---- spectral probes (spectral.cpp) --------------------------------------------- */
+int chebfd_lanczos_bounds(chebfd_matrix* a, int iters, uint64_t seed, double* lo,
+                          double* hi);                                 /* :96-154 */
+/* mu[0..order] raw KPM moments (spectral.cpp:156-205) */
+int chebfd_kpm_dos(chebfd_matrix* a, double bounds_lo, double bounds_hi, int order,
+                   int num_samples, uint64_t seed, double* mu);
+/* Jackson-damped count integral (ChebSeriesDensity::count, spectral.cpp:46-57) */
+int chebfd_dos_count(const double* mu, int order, double bounds_lo, double bounds_hi, double lo,
+                     double hi, double* out);
+
+/* ---- full ChebFD driver (solver.cpp:93-214) ------------------------------------- */
+typedef struct {
+    double target_lo, target_hi;
+    double epsilon;         /* 1e-10 */
+    int n_search;           /* 0 = 2*ceil(N_T estimate) */
+    int degree;             /* 0 = choose_parameters (filter_design.cpp:356-369) */
+    int kernel, kernel_mu;  /* Lanczos, 2 */
+    int max_iters;          /* 40 */
+    uint64_t seed;          /* 1 */
+    int dos_moments;        /* 2000 */
+    int dos_samples;        /* 32 */
+    double bounds_lo, bounds_hi; /* lo >= hi: Lanczos bounds */
+    int collect_weight_density;  /* 1 */
+} chebfd_solver_options;
+
+void chebfd_solver_options_default(chebfd_solver_options* o);
+
+typedef struct {
+    int converged, iterations, n_search, degree, n_values;
+    double total_spmvms, sigma, eta, bounds_lo, bounds_hi, matrix_norm_est, n_target_estimate;
+    double seconds, weight_integral;
+} chebfd_solve_report;
+
+/* values/residual_norms/accepted: capacity `cap` >= n_search; history:
+ * max_iters x 5 (iteration, min_residual, max_residual, accepted,
+ * cumulative_spmvms) or NULL; weight_moments: (degree+1) or NULL (summed
+ * moments of the last filter, WeightDensity input); vectors: if non-NULL
+ * receives a new block with the final Ritz vectors. */
+int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* opts, chebfd_solve_report* rep,
+                 int cap, double* values, double* residual_norms, int* accepted,
+                 double* history, chebfd_block** vectors);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHEBFD_B200_H */

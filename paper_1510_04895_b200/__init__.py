@@ -1,0 +1,19 @@
+"""chebfd_b200: B200-native ChebFD hot path (arXiv 1510.04895).
+
+The product is libchebfd_b200.so (csrc/, sm_100a kernels + C ABI declared in
+include/chebfd_b200.h).  This package mirrors the reference's driver API on
+top of that ABI; it never computes on the CPU.
+"""
+from .api import (  # noqa: F401
+    BlockVector, ChebfdError, Context, ConvergenceReport, CudaError, DomainError, DosEstimate,
+    FilterPolynomial, Interval, InvalidArgument, Kernel, LatticeSpec, MomentTable, NcclError,
+    NumericalError, OutOfRange, RitzSet, SolverOptions, SparseMatrix, SvqbResult, Unsupported,
+    apply_filter, apply_filter_host, block_axpy_scal, block_mult_small, column_dots, column_norms,
+    csr_graphene, csr_topological_insulator, estimate_count, eval_scalar, gram, intensity_model,
+    kernel_coeffs, kpm_dos, lanczos_bounds, make_filter, per_row_bytes, per_row_flops,
+    rayleigh_ritz, recurrence_step, solve, spmmvm, spmmvm_fused, svqb_orthonormalize,
+    window_coeffs,
+)
+from ._lib import LIB_PATH, load  # noqa: F401
+
+__version__ = "0.1.0"

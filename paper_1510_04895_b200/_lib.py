@@ -1,0 +1,128 @@
+"""ctypes binding of libchebfd_b200.so (the C ABI in include/chebfd_b200.h).
+
+The shared library is built in tree (``make -C paper_1510_04895_b200/csrc``
+or ``__graft_entry__.build()``).  There is no fallback: if the library is
+missing or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libchebfd_b200.so")
+
+_i64 = C.c_int64
+_u64 = C.c_uint64
+_dbl = C.c_double
+_vp = C.c_void_p
+_int = C.c_int
+_pp = C.POINTER(C.c_void_p)
+
+
+class chebfd_lattice(C.Structure):
+    _fields_ = [("lx", _i64), ("ly", _i64), ("lz", _i64), ("t", _dbl), ("disorder", _dbl),
+                ("boundary", _int), ("seed", _u64)]
+
+
+class chebfd_matrix_info(C.Structure):
+    _fields_ = [("kind", _int), ("dim", _i64), ("nnz", _i64), ("local_rows", _i64),
+                ("row_begin", _i64), ("local_nnz", _i64), ("sell_entries", _i64),
+                ("halo_lo", _i64), ("halo_hi", _i64), ("chunk", _int), ("max_row_len", _int)]
+
+
+class chebfd_solver_options(C.Structure):
+    _fields_ = [("target_lo", _dbl), ("target_hi", _dbl), ("epsilon", _dbl), ("n_search", _int),
+                ("degree", _int), ("kernel", _int), ("kernel_mu", _int), ("max_iters", _int),
+                ("seed", _u64), ("dos_moments", _int), ("dos_samples", _int),
+                ("bounds_lo", _dbl), ("bounds_hi", _dbl), ("collect_weight_density", _int)]
+
+
+class chebfd_solve_report(C.Structure):
+    _fields_ = [("converged", _int), ("iterations", _int), ("n_search", _int), ("degree", _int),
+                ("n_values", _int), ("total_spmvms", _dbl), ("sigma", _dbl), ("eta", _dbl),
+                ("bounds_lo", _dbl), ("bounds_hi", _dbl), ("matrix_norm_est", _dbl),
+                ("n_target_estimate", _dbl), ("seconds", _dbl), ("weight_integral", _dbl)]
+
+
+_SIGS = {
+    "chebfd_last_error": (C.c_char_p, []),
+    "chebfd_version": (C.c_char_p, []),
+    "chebfd_nccl_unique_id": (_int, [_vp]),
+    "chebfd_ctx_create": (_int, [_int, _pp]),
+    "chebfd_ctx_create_dist": (_int, [_int, _int, _int, _vp, _pp]),
+    "chebfd_ctx_destroy": (_int, [_vp]),
+    "chebfd_ctx_synchronize": (_int, [_vp]),
+    "chebfd_ctx_stream": (_int, [_vp, _pp]),
+    "chebfd_ctx_info": (_int, [_vp, _vp, _vp, _vp, _vp]),
+    "chebfd_ctx_launch_count": (_int, [_vp, _vp]),
+    "chebfd_ctx_set_option": (_int, [_vp, _int, _i64]),
+    "chebfd_ctx_event_record": (_int, [_vp, _int]),
+    "chebfd_ctx_event_elapsed": (_int, [_vp, _int, _int, _vp]),
+    "chebfd_host_alloc": (_int, [C.c_size_t, _pp]),
+    "chebfd_host_free": (_int, [_vp]),
+    "chebfd_csr_graphene": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "chebfd_csr_topological_insulator": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "chebfd_matrix_from_csr": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _pp]),
+    "chebfd_matrix_graphene": (_int, [_vp, _vp, _pp]),
+    "chebfd_matrix_topological_insulator": (_int, [_vp, _vp, _pp]),
+    "chebfd_matrix_destroy": (_int, [_vp]),
+    "chebfd_matrix_get_info": (_int, [_vp, _vp]),
+    "chebfd_block_create": (_int, [_vp, _i64, _pp]),
+    "chebfd_block_create_dim": (_int, [_vp, _int, _i64, _i64, _pp]),
+    "chebfd_block_destroy": (_int, [_vp]),
+    "chebfd_block_info": (_int, [_vp, _vp, _vp, _vp, _vp]),
+    "chebfd_block_upload": (_int, [_vp, _vp]),
+    "chebfd_block_download": (_int, [_vp, _vp]),
+    "chebfd_block_copy": (_int, [_vp, _vp]),
+    "chebfd_block_zero": (_int, [_vp]),
+    "chebfd_block_randomize": (_int, [_vp, _u64]),
+    "chebfd_block_randomize_device": (_int, [_vp, _u64]),
+    "chebfd_block_scale_columns": (_int, [_vp, _vp]),
+    "chebfd_block_copy_columns": (_int, [_vp, _i64, _vp, _i64, _i64]),
+    "chebfd_block_device_ptr": (_int, [_vp, _pp]),
+    "chebfd_spmmvm": (_int, [_vp, _vp, _vp, _dbl, _dbl]),
+    "chebfd_spmmvm_fused": (_int, [_vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp]),
+    "chebfd_recurrence_step": (_int, [_vp, _vp, _vp, _dbl, _dbl]),
+    "chebfd_block_axpy_scal": (_int, [_vp, _vp, _vp, _dbl, _dbl, _dbl]),
+    "chebfd_column_dots": (_int, [_vp, _vp, _vp]),
+    "chebfd_column_norms": (_int, [_vp, _vp]),
+    "chebfd_gram": (_int, [_vp, _vp, _vp]),
+    "chebfd_block_mult_small": (_int, [_vp, _vp, _i64, _vp]),
+    "chebfd_window_coeffs": (_int, [_dbl, _dbl, _dbl, _dbl, _int, _vp]),
+    "chebfd_kernel_coeffs": (_int, [_int, _int, _int, _vp]),
+    "chebfd_make_filter": (_int, [_dbl, _dbl, _dbl, _dbl, _int, _int, _int, _vp, _vp, _vp]),
+    "chebfd_eval_scalar": (_int, [_vp, _int, _dbl, _dbl, _dbl, _dbl, _dbl, _vp]),
+    "chebfd_apply_filter": (_int, [_vp, _vp, _vp, _int, _dbl, _dbl, _vp]),
+    "chebfd_apply_filter_host": (_int, [_vp, _vp, _i64, _vp, _int, _dbl, _dbl, _vp]),
+    "chebfd_svqb": (_int, [_vp, _dbl, _vp, _vp]),
+    "chebfd_rayleigh_ritz": (_int, [_vp, _vp, _vp, _vp, _vp]),
+    "chebfd_lanczos_bounds": (_int, [_vp, _int, _u64, _vp, _vp]),
+    "chebfd_kpm_dos": (_int, [_vp, _dbl, _dbl, _int, _int, _u64, _vp]),
+    "chebfd_dos_count": (_int, [_vp, _int, _dbl, _dbl, _dbl, _dbl, _vp]),
+    "chebfd_solver_options_default": (None, [_vp]),
+    "chebfd_solve": (_int, [_vp, _vp, _vp, _int, _vp, _vp, _vp, _vp, _pp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the library once; raise ImportError if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not found: build the CUDA library first "
+            "(python -c 'import __graft_entry__ as g; g.build()' or "
+            "make -C paper_1510_04895_b200/csrc)")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

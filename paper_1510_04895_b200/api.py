@@ -1,0 +1,725 @@
+"""Python mirror of the reference's ChebFD driver API, backed by the sm_100a
+library through its C ABI (include/chebfd_b200.h).
+
+Names, argument meaning and error behaviour follow the reference's C++ API
+(/root/reference/proj/include/chebfd/*.hpp); every device call goes through
+libchebfd_b200.so -- there is no CPU fallback.  C++ exception types map to
+Python exceptions: std::invalid_argument -> InvalidArgument (ValueError),
+std::runtime_error -> NumericalError (RuntimeError), std::domain_error ->
+DomainError (ValueError), std::out_of_range -> OutOfRange (IndexError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+REAL64, COMPLEX128 = 0, 1
+BOUNDARY = {"periodic_xy_open_z": 0, "periodic_all": 1, "open_all": 2}
+KERNELS = {"none": 0, "fejer": 1, "jackson": 2, "lanczos": 3}
+
+
+# ------------------------------------------------------------------ errors --
+class ChebfdError(Exception):
+    code = -1
+
+
+class InvalidArgument(ChebfdError, ValueError):
+    code = 1
+
+
+class NumericalError(ChebfdError, RuntimeError):
+    code = 2
+
+
+class DomainError(ChebfdError, ValueError):
+    code = 3
+
+
+class OutOfRange(ChebfdError, IndexError):
+    code = 4
+
+
+class CudaError(ChebfdError, RuntimeError):
+    code = 5
+
+
+class NcclError(ChebfdError, RuntimeError):
+    code = 6
+
+
+class Unsupported(ChebfdError, NotImplementedError):
+    code = 7
+
+
+_EXC = {c.code: c for c in (InvalidArgument, NumericalError, DomainError, OutOfRange, CudaError,
+                            NcclError, Unsupported)}
+
+
+def _lib():
+    return L.load()
+
+
+def _check(rc):
+    if rc:
+        msg = _lib().chebfd_last_error().decode()
+        raise _EXC.get(rc, ChebfdError)(msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ----------------------------------------------------------------- context --
+class Context:
+    """One GPU, one stream (replaces the reference's OpenMP runtime,
+    parallel.hpp:18-54).  ``Context.distributed(rank, nranks, uid)`` joins a
+    row-partitioned multi-GPU context (one process per GPU)."""
+
+    def __init__(self, device: int = 0, _handle=None):
+        self._h = C.c_void_p()
+        if _handle is None:
+            _check(_lib().chebfd_ctx_create(device, C.byref(self._h)))
+        else:
+            self._h = _handle
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(_lib().chebfd_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def distributed(cls, device: int, rank: int, nranks: int, uid: bytes):
+        h = C.c_void_p()
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        _check(_lib().chebfd_ctx_create_dist(device, rank, nranks, buf, C.byref(h)))
+        return cls(_handle=h)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib().chebfd_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(_lib().chebfd_ctx_synchronize(self._h))
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(_lib().chebfd_ctx_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def info(self):
+        d, r, n, s = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(_lib().chebfd_ctx_info(self._h, C.byref(d), C.byref(r), C.byref(n), C.byref(s)))
+        return dict(device=d.value, rank=r.value, nranks=n.value, num_sms=s.value)
+
+    @property
+    def launch_count(self) -> int:
+        v = C.c_int64()
+        _check(_lib().chebfd_ctx_launch_count(self._h, C.byref(v)))
+        return v.value
+
+    def record(self, slot: int):
+        """Record CUDA event `slot` (0..15) on the context stream."""
+        _check(_lib().chebfd_ctx_event_record(self._h, slot))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        _check(_lib().chebfd_ctx_event_elapsed(self._h, a, b, C.byref(ms)))
+        return ms.value
+
+    def set_option(self, name: str, value):
+        code = {"graphs": 1, "overlap": 2}[name]
+        _check(_lib().chebfd_ctx_set_option(self._h, code, int(value)))
+
+
+# ------------------------------------------------------------- intervals --
+@dataclass
+class Interval:
+    """filter.hpp:19-26"""
+    lo: float = 0.0
+    hi: float = 0.0
+
+    def width(self):
+        return self.hi - self.lo
+
+    def half_width(self):
+        return 0.5 * (self.hi - self.lo)
+
+    def center(self):
+        return 0.5 * (self.lo + self.hi)
+
+    def contains(self, x):
+        if isinstance(x, Interval):
+            return self.lo <= x.lo and x.hi <= self.hi
+        return self.lo <= x <= self.hi
+
+
+def _iv(x) -> Interval:
+    return x if isinstance(x, Interval) else Interval(float(x[0]), float(x[1]))
+
+
+@dataclass
+class Kernel:
+    """Damping kernel (filter.hpp:12-17): kind in none/fejer/jackson/lanczos."""
+    kind: str = "lanczos"
+    mu: int = 2
+
+    def name(self) -> str:
+        return f"lanczos{self.mu}" if self.kind == "lanczos" else self.kind
+
+    @staticmethod
+    def parse(s: str) -> "Kernel":
+        if s in ("none", "fejer", "jackson"):
+            return Kernel(s, 0)
+        if s.startswith("lanczos"):
+            mu = int(s[7:]) if len(s) > 7 else 2
+            if mu < 1:
+                raise InvalidArgument("lanczos kernel needs mu >= 1")
+            return Kernel("lanczos", mu)
+        raise InvalidArgument("unknown kernel: " + s)
+
+    def code(self):
+        return KERNELS[self.kind], self.mu
+
+
+def _kernel(k) -> Kernel:
+    return k if isinstance(k, Kernel) else Kernel.parse(k)
+
+
+@dataclass
+class LatticeSpec:
+    """models.hpp:19-29 (onsite_potential not supported)."""
+    lx: int = 1
+    ly: int = 1
+    lz: int = 1
+    t: float = 1.0
+    disorder: float = 0.0
+    boundary: str = "periodic_xy_open_z"
+    seed: int = 1
+
+    def _c(self):
+        return L.chebfd_lattice(self.lx, self.ly, self.lz, self.t, self.disorder,
+                                BOUNDARY[self.boundary], self.seed)
+
+
+# ---------------------------------------------------------- host CSR gen --
+def csr_graphene(spec: LatticeSpec, row_begin=0, row_end=None):
+    """Host CSR of graphene() rows (models.cpp:142-178), stencil-direct."""
+    return _csr(_lib().chebfd_csr_graphene, spec, row_begin, row_end, np.float64)
+
+
+def csr_topological_insulator(spec: LatticeSpec, row_begin=0, row_end=None):
+    """Host CSR of topological_insulator() rows (models.cpp:80-140)."""
+    return _csr(_lib().chebfd_csr_topological_insulator, spec, row_begin, row_end, np.complex128)
+
+
+def _csr(fn, spec, r0, r1, dtype):
+    s = spec._c()
+    dim, nnz = C.c_int64(), C.c_int64()
+    if r1 is None:
+        _check(fn(C.byref(s), 0, 0, C.byref(dim), C.byref(nnz), None, None, None))
+        r1 = dim.value
+    _check(fn(C.byref(s), r0, r1, C.byref(dim), C.byref(nnz), None, None, None))
+    offs = np.empty(r1 - r0 + 1, np.int64)
+    cols = np.empty(nnz.value, np.int64)
+    vals = np.empty(nnz.value, dtype)
+    _check(fn(C.byref(s), r0, r1, C.byref(dim), C.byref(nnz), _ptr(offs), _ptr(cols), _ptr(vals)))
+    return offs, cols, vals
+
+
+# ----------------------------------------------------------- sparse matrix --
+class SparseMatrix:
+    """Device SELL-C-sigma matrix (C = 32, sigma = 1); replaces
+    SparseMatrix<S> (sparse_matrix.hpp:15-107)."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self._h = handle
+        info = L.chebfd_matrix_info()
+        _check(_lib().chebfd_matrix_get_info(self._h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in L.chebfd_matrix_info._fields_}
+
+    @classmethod
+    def from_csr(cls, ctx, dim, row_offsets, col_indices, values):
+        offs = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        cols = np.ascontiguousarray(col_indices, dtype=np.int64)
+        vals = np.ascontiguousarray(values)
+        if len(offs) != dim + 1:
+            raise InvalidArgument("SparseMatrix: row_offsets length must be dim+1")
+        if len(cols) != len(vals):
+            raise InvalidArgument("SparseMatrix: col/value length mismatch")
+        if offs[-1] != len(vals):
+            raise InvalidArgument("SparseMatrix: invalid row_offsets range")
+        kind = COMPLEX128 if np.iscomplexobj(vals) else REAL64
+        vals = vals.astype(np.complex128 if kind else np.float64, copy=False)
+        h = C.c_void_p()
+        _check(_lib().chebfd_matrix_from_csr(ctx._h, kind, dim, _ptr(offs), _ptr(cols), _ptr(vals),
+                                              C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def graphene(cls, ctx, spec: LatticeSpec):
+        h = C.c_void_p()
+        s = spec._c()
+        _check(_lib().chebfd_matrix_graphene(ctx._h, C.byref(s), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def topological_insulator(cls, ctx, spec: LatticeSpec):
+        h = C.c_void_p()
+        s = spec._c()
+        _check(_lib().chebfd_matrix_topological_insulator(ctx._h, C.byref(s), C.byref(h)))
+        return cls(ctx, h)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib().chebfd_matrix_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def dim(self):
+        return self.info["dim"]
+
+    def nnz(self):
+        return self.info["nnz"]
+
+    @property
+    def kind(self):
+        return self.info["kind"]
+
+    @property
+    def dtype(self):
+        return np.complex128 if self.kind else np.float64
+
+    def avg_nonzeros_per_row(self):
+        return self.nnz() / self.dim() if self.dim() else 0.0
+
+    @property
+    def local_rows(self):
+        return self.info["local_rows"]
+
+    @property
+    def row_begin(self):
+        return self.info["row_begin"]
+
+
+# ------------------------------------------------------------ block vector --
+class BlockVector:
+    """Device D x n_b row-major block (block_vector.hpp:17-102).  Created
+    conforming to a matrix (owned rows of this rank, halo storage for
+    gathers) or free-standing by (ctx, dim, width, kind)."""
+
+    def __init__(self, A: Optional[SparseMatrix] = None, width: int = 1, *, ctx=None, dim=None,
+                 kind=None, _handle=None):
+        self.A = A
+        if _handle is not None:
+            self._h = _handle
+        elif A is not None:
+            self._h = C.c_void_p()
+            _check(_lib().chebfd_block_create(A._h, width, C.byref(self._h)))
+        else:
+            self._h = C.c_void_p()
+            _check(_lib().chebfd_block_create_dim(ctx._h, kind, dim, width, C.byref(self._h)))
+        self.ctx = ctx if ctx is not None else A.ctx
+        k, r, w, rb = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        _check(_lib().chebfd_block_info(self._h, C.byref(k), C.byref(r), C.byref(w), C.byref(rb)))
+        self.kind, self.rows, self.width_, self.row_begin = k.value, r.value, w.value, rb.value
+
+    @classmethod
+    def like(cls, other: "BlockVector", width=None):
+        w = other.width_ if width is None else width
+        if other.A is not None:
+            return cls(other.A, w)
+        return cls(ctx=other.ctx, dim=other.rows, width=w, kind=other.kind)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib().chebfd_block_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def dim(self):
+        return self.rows
+
+    def width(self):
+        return self.width_
+
+    @property
+    def dtype(self):
+        return np.complex128 if self.kind else np.float64
+
+    @property
+    def shape(self):
+        return (self.rows, self.width_)
+
+    def upload(self, host: np.ndarray):
+        a = np.ascontiguousarray(host, dtype=self.dtype)
+        if a.shape != self.shape:
+            raise InvalidArgument(f"upload: shape {a.shape} != {self.shape}")
+        _check(_lib().chebfd_block_upload(self._h, _ptr(a)))
+        return self
+
+    def to_numpy(self) -> np.ndarray:
+        out = np.empty(self.shape, dtype=self.dtype)
+        _check(_lib().chebfd_block_download(self._h, _ptr(out)))
+        return out
+
+    def copy_from(self, other: "BlockVector"):
+        _check(_lib().chebfd_block_copy(self._h, other._h))
+        return self
+
+    def zero(self):
+        _check(_lib().chebfd_block_zero(self._h))
+        return self
+
+    def randomize(self, seed: int):
+        """BlockVector::randomize (block_vector.hpp:42-51), same stream."""
+        _check(_lib().chebfd_block_randomize(self._h, seed))
+        return self
+
+    def randomize_device(self, seed: int):
+        """Fast device Gaussian fill (Philox) -- not the reference stream."""
+        _check(_lib().chebfd_block_randomize_device(self._h, seed))
+        return self
+
+    def scale_columns(self, s):
+        s = np.ascontiguousarray(s, dtype=np.float64)
+        _check(_lib().chebfd_block_scale_columns(self._h, _ptr(s)))
+        return self
+
+    def copy_columns(self, d0, src: "BlockVector", s0, n):
+        _check(_lib().chebfd_block_copy_columns(self._h, d0, src._h, s0, n))
+        return self
+
+    @property
+    def device_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(_lib().chebfd_block_device_ptr(self._h, C.byref(p)))
+        return p.value
+
+
+# ------------------------------------------------------------------ kernels --
+def spmmvm(A: SparseMatrix, X: BlockVector, alpha: float, beta: float) -> BlockVector:
+    """Y = (alpha A + beta I) X  (kernels.hpp:45-69)."""
+    Y = BlockVector.like(X)
+    _check(_lib().chebfd_spmmvm(A._h, X._h, Y._h, alpha, beta))
+    return Y
+
+
+def spmmvm_fused(A, U, W, X, alpha, beta, coeff, dots: bool = False):
+    """W <- 2(alpha A + beta)U - W;  X <- X + coeff W  (kernels.hpp:71-118).
+    Returns d_k = <x_k(before), w_k(after)> when dots=True."""
+    d = np.empty(U.width_, dtype=U.dtype) if dots else None
+    _check(_lib().chebfd_spmmvm_fused(A._h, U._h, W._h, X._h, alpha, beta, coeff, _ptr(d)))
+    return d
+
+
+def recurrence_step(A, U, W, alpha, beta):
+    """W <- 2(alpha A + beta)U - W  (kernels.hpp:120-145)."""
+    _check(_lib().chebfd_recurrence_step(A._h, U._h, W._h, alpha, beta))
+
+
+def block_axpy_scal(X, U, W, c0, c1, c2):
+    """X <- c0 X + c1 U + c2 W  (kernels.hpp:147-162)."""
+    _check(_lib().chebfd_block_axpy_scal(X._h, U._h, W._h, c0, c1, c2))
+
+
+def column_dots(X, Y) -> np.ndarray:
+    """d_k = <x_k, y_k>  (kernels.hpp:194-213)."""
+    d = np.empty(X.width_, dtype=X.dtype)
+    _check(_lib().chebfd_column_dots(X._h, Y._h, _ptr(d)))
+    return d
+
+
+def column_norms(X) -> np.ndarray:
+    out = np.empty(X.width_)
+    _check(_lib().chebfd_column_norms(X._h, _ptr(out)))
+    return out
+
+
+def gram(X, Y) -> np.ndarray:
+    """G(k,l) = <x_k, y_l>  (kernels.hpp:164-192)."""
+    g = np.empty((X.width_, Y.width_), dtype=X.dtype)
+    _check(_lib().chebfd_gram(X._h, Y._h, _ptr(g)))
+    return g
+
+
+def block_mult_small(X, B) -> BlockVector:
+    """Y = X B with a small dense B  (kernels.hpp:215-232)."""
+    B = np.ascontiguousarray(B, dtype=X.dtype)
+    if B.ndim != 2 or B.shape[0] != X.width_:
+        raise InvalidArgument("block_mult_small: shape mismatch")
+    Y = BlockVector.like(X, width=B.shape[1])
+    _check(_lib().chebfd_block_mult_small(X._h, _ptr(B), B.shape[1], Y._h))
+    return Y
+
+
+# ------------------------------------------------------------------ filter --
+def window_coeffs(target, bounds, degree: int) -> np.ndarray:
+    t, b = _iv(target), _iv(bounds)
+    out = np.empty(max(degree, 0) + 1)
+    _check(_lib().chebfd_window_coeffs(t.lo, t.hi, b.lo, b.hi, degree, _ptr(out)))
+    return out
+
+
+def kernel_coeffs(kernel, degree: int) -> np.ndarray:
+    k, mu = _kernel(kernel).code()
+    out = np.empty(max(degree, 0) + 1)
+    _check(_lib().chebfd_kernel_coeffs(k, mu, degree, _ptr(out)))
+    return out
+
+
+@dataclass
+class FilterPolynomial:
+    """filter.hpp:39-46"""
+    degree: int = 0
+    combined: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    alpha: float = 1.0
+    beta: float = 0.0
+    target: Interval = field(default_factory=Interval)
+    bounds: Interval = field(default_factory=Interval)
+    kernel: Kernel = field(default_factory=Kernel)
+
+
+def make_filter(target, bounds, degree: int, kernel="lanczos2") -> FilterPolynomial:
+    """combined[n] = g_n c_n  (filter.cpp:86-99)."""
+    t, b, k = _iv(target), _iv(bounds), _kernel(kernel)
+    kk, mu = k.code()
+    comb = np.empty(max(degree, 0) + 1)
+    a, be = C.c_double(), C.c_double()
+    _check(_lib().chebfd_make_filter(t.lo, t.hi, b.lo, b.hi, degree, kk, mu, _ptr(comb),
+                                     C.byref(a), C.byref(be)))
+    return FilterPolynomial(degree, comb, a.value, be.value, t, b, k)
+
+
+def eval_scalar(p: FilterPolynomial, x: float) -> float:
+    out = C.c_double()
+    comb = np.ascontiguousarray(p.combined, dtype=np.float64)
+    _check(_lib().chebfd_eval_scalar(_ptr(comb), p.degree, p.alpha, p.beta, p.bounds.lo,
+                                     p.bounds.hi, x, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class MomentTable:
+    """filter.hpp:61-68: m(n,k) = <x_k, T_n(alpha A + beta) x_k>."""
+    degree: int
+    width: int
+    m: np.ndarray  # (degree+1, width)
+
+    def __call__(self, n, k):
+        return self.m[n, k]
+
+
+def apply_filter(A: SparseMatrix, X: BlockVector, p: FilterPolynomial,
+                 want_moments: bool = False) -> Optional[MomentTable]:
+    """X <- p[A] X in exactly Np*n_b column spMVMs (filter.hpp:73-116)."""
+    comb = np.ascontiguousarray(p.combined, dtype=np.float64)
+    if len(comb) < p.degree + 1 and p.degree >= 2:
+        raise InvalidArgument("apply_filter: coefficient array shorter than degree+1")
+    mom = np.empty((max(p.degree, 0) + 1, X.width_)) if want_moments else None
+    _check(_lib().chebfd_apply_filter(A._h, X._h, _ptr(comb), p.degree, p.alpha, p.beta,
+                                      _ptr(mom)))
+    return MomentTable(p.degree, X.width_, mom) if want_moments else None
+
+
+def apply_filter_host(A: SparseMatrix, x: np.ndarray, p: FilterPolynomial,
+                      want_moments: bool = False):
+    """End-to-end filter of a HOST block (in place): H2D, filter, D2H."""
+    if x.dtype != A.dtype or not x.flags.c_contiguous:
+        raise InvalidArgument("apply_filter_host: x must be C-contiguous of the matrix dtype")
+    comb = np.ascontiguousarray(p.combined, dtype=np.float64)
+    mom = np.empty((p.degree + 1, x.shape[1])) if want_moments else None
+    _check(_lib().chebfd_apply_filter_host(A._h, _ptr(x), x.shape[1], _ptr(comb), p.degree,
+                                           p.alpha, p.beta, _ptr(mom)))
+    return MomentTable(p.degree, x.shape[1], mom) if want_moments else None
+
+
+# ------------------------------------------------------------------ solver --
+@dataclass
+class SvqbResult:
+    q: BlockVector
+    rank: int
+
+
+def svqb_orthonormalize(Y: BlockVector, drop_tol: float = 1e-14) -> SvqbResult:
+    """solver.cpp:32-61.  q keeps Y's width; columns >= rank are zero."""
+    Q = BlockVector.like(Y)
+    r = C.c_int64()
+    _check(_lib().chebfd_svqb(Y._h, drop_tol, Q._h, C.byref(r)))
+    return SvqbResult(Q, r.value)
+
+
+@dataclass
+class RitzSet:
+    """solver.hpp:27-33"""
+    values: np.ndarray
+    vectors: Optional[BlockVector]
+    residual_norms: np.ndarray
+    accepted: np.ndarray
+
+
+def rayleigh_ritz(A: SparseMatrix, Q: BlockVector) -> RitzSet:
+    """solver.cpp:63-91"""
+    V = BlockVector.like(Q)
+    vals = np.empty(Q.width_)
+    res = np.empty(Q.width_)
+    _check(_lib().chebfd_rayleigh_ritz(A._h, Q._h, V._h, _ptr(vals), _ptr(res)))
+    return RitzSet(vals, V, res, np.zeros(Q.width_, dtype=bool))
+
+
+def lanczos_bounds(A: SparseMatrix, iters: int = 30, seed: int = 1) -> Interval:
+    """spectral.cpp:96-154"""
+    lo, hi = C.c_double(), C.c_double()
+    _check(_lib().chebfd_lanczos_bounds(A._h, iters, seed, C.byref(lo), C.byref(hi)))
+    return Interval(lo.value, hi.value)
+
+
+@dataclass
+class DosEstimate:
+    """spectral.hpp:55-79 (Jackson-damped Chebyshev moments)."""
+    moments: np.ndarray
+    bounds: Interval
+    num_samples: int = 0
+    matrix_dim: int = 0
+
+    def count(self, lo, hi) -> float:
+        mu = np.ascontiguousarray(self.moments, dtype=np.float64)
+        out = C.c_double()
+        _check(_lib().chebfd_dos_count(_ptr(mu), len(mu) - 1, self.bounds.lo, self.bounds.hi,
+                                       lo, hi, C.byref(out)))
+        return out.value
+
+
+def kpm_dos(A: SparseMatrix, bounds, order: int, num_samples: int, seed: int = 1) -> DosEstimate:
+    """spectral.cpp:156-205"""
+    b = _iv(bounds)
+    mu = np.empty(max(order, 0) + 1)
+    _check(_lib().chebfd_kpm_dos(A._h, b.lo, b.hi, order, num_samples, seed, _ptr(mu)))
+    return DosEstimate(mu, b, num_samples, A.dim())
+
+
+def estimate_count(dos: DosEstimate, interval) -> float:
+    """spectral.cpp:90-94"""
+    iv = _iv(interval)
+    if not dos.bounds.contains(iv):
+        raise InvalidArgument("estimate_count: interval outside DOS bounds")
+    return dos.count(iv.lo, iv.hi)
+
+
+@dataclass
+class SolverOptions:
+    """solver.hpp:12-25"""
+    target: Interval = field(default_factory=Interval)
+    epsilon: float = 1e-10
+    n_search: int = 0
+    degree: int = 0
+    kernel: Kernel = field(default_factory=lambda: Kernel("lanczos", 2))
+    max_iters: int = 40
+    seed: int = 1
+    dos_moments: int = 2000
+    dos_samples: int = 32
+    deterministic: bool = True
+    bounds: Interval = field(default_factory=Interval)
+    collect_weight_density: bool = True
+
+
+@dataclass
+class ConvergenceReport:
+    """solver.hpp:43-60"""
+    converged: bool
+    iterations: int
+    total_spmvms: float
+    n_search: int
+    degree: int
+    sigma: float
+    eta: float
+    bounds: Interval
+    matrix_norm_est: float
+    n_target_estimate: float
+    ritz: RitzSet
+    history: np.ndarray
+    weight_integral: float
+    have_weight: bool
+    seconds: float
+
+
+def solve(A: SparseMatrix, opts: SolverOptions) -> ConvergenceReport:
+    """Full ChebFD iteration (solver.cpp:93-214) driven from host C++ with all
+    block work on the device."""
+    o = L.chebfd_solver_options()
+    _lib().chebfd_solver_options_default(C.byref(o))
+    t = _iv(opts.target)
+    b = _iv(opts.bounds)
+    kk, mu = _kernel(opts.kernel).code()
+    o.target_lo, o.target_hi = t.lo, t.hi
+    o.epsilon = opts.epsilon
+    o.n_search = opts.n_search
+    o.degree = opts.degree
+    o.kernel, o.kernel_mu = kk, mu
+    o.max_iters = opts.max_iters
+    o.seed = opts.seed
+    o.dos_moments = opts.dos_moments
+    o.dos_samples = opts.dos_samples
+    o.bounds_lo, o.bounds_hi = b.lo, b.hi
+    o.collect_weight_density = int(opts.collect_weight_density)
+    rep = L.chebfd_solve_report()
+    cap = max(4096, 2 * opts.n_search)
+    vals = np.zeros(cap)
+    res = np.zeros(cap)
+    acc = np.zeros(cap, dtype=np.int32)
+    hist = np.zeros((opts.max_iters, 5))
+    vh = C.c_void_p()
+    _check(_lib().chebfd_solve(A._h, C.byref(o), C.byref(rep), cap, _ptr(vals), _ptr(res),
+                               _ptr(acc), _ptr(hist), C.byref(vh)))
+    n = rep.n_values
+    V = BlockVector(A, _handle=vh) if vh.value else None
+    ritz = RitzSet(vals[:n].copy(), V, res[:n].copy(), acc[:n].astype(bool))
+    return ConvergenceReport(bool(rep.converged), rep.iterations, rep.total_spmvms, rep.n_search,
+                             rep.degree, rep.sigma, rep.eta, Interval(rep.bounds_lo, rep.bounds_hi),
+                             rep.matrix_norm_est, rep.n_target_estimate, ritz,
+                             hist[:rep.iterations].copy(), rep.weight_integral,
+                             bool(opts.collect_weight_density), rep.seconds)
+
+
+# ----------------------------------------------------- bench conventions --
+def per_row_flops(n_nzr, f_a, f_m):
+    """bench.cpp:28-30"""
+    return n_nzr * (f_a + f_m) + np.ceil(9.0 * f_a / 2.0) + np.ceil(11.0 * f_m / 2.0)
+
+
+def per_row_bytes(n_nzr, s_d, s_i, n_b):
+    """bench.cpp:32-34"""
+    return n_nzr / n_b * (s_d + s_i) + 5.0 * s_d
+
+
+def intensity_model(n_nzr, s_d, s_i, f_a, f_m, n_b):
+    """bench.cpp:38-42"""
+    if n_b < 1:
+        raise InvalidArgument("intensity_model: block size must be >= 1")
+    if not n_nzr > 0:
+        raise InvalidArgument("intensity_model: N_nzr must be positive")
+    return per_row_flops(n_nzr, f_a, f_m) / per_row_bytes(n_nzr, s_d, s_i, n_b)

@@ -1,0 +1,58 @@
+// Helpers shared by the C-ABI translation units (capi.cu, solver.cu, blas.cu).
+#pragma once
+
+#include <string>
+
+#include "internal.hpp"
+
+namespace cfd {
+
+extern thread_local std::string g_last_error;
+
+// Run f, translating internal exceptions into status codes (ABI boundary).
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return CHEBFD_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("host allocation failed: ") + e.what();
+        return CHEBFD_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return CHEBFD_ERR_RUNTIME;
+    }
+}
+
+void cublas_check(int st, const char* what);
+void nccl_check(int st, const char* what);
+void ctx_sync(Context& c);
+std::unique_ptr<Block> make_block(Context& c, const Matrix* m, int kind, int64_t rows,
+                                  int64_t width);
+void check_same_shape(const Block& x, const Block& y);
+void check_conforms(const Matrix& a, const Block& x, const char* who);
+void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered);
+void allreduce_sum(Context& c, double* dev, size_t n, cudaStream_t st);
+void column_dots_host(Context& c, const Block& x, const Block& y, void* out);
+void gram_host(Context& c, const Block& x, const Block& y, void* out);
+void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* combined, int degree,
+                         double alpha, double beta, double* moments_host);
+
+// blas.cu: cuBLAS / cuSOLVER wrappers on row-major blocks
+// dev_out (row-major nx x ny, local rows only) = X^H Y
+void gemm_gram(Context& c, const Block& x, const Block& y, void* dev_out);
+// Y = X B with B given on the host (row-major nb x bcols)
+void mult_small_host_b(Context& c, const Block& x, const void* b_host, int64_t bcols, Block& y);
+// Y = X B with B on the device (row-major)
+void mult_small_dev_b(Context& c, const Block& x, const void* b_dev, int64_t bcols, Block& y);
+// Hermitian eigendecomposition of a host row-major n x n matrix (already
+// symmetrised): ascending eigenvalues, row-major eigenvectors (columns).
+// Returns false if the solver reports failure.
+bool heev_host(Context& c, int kind, int64_t n, const void* a_rowmajor, double* w, void* v_rowmajor,
+               bool vectors);
+void destroy_cusolver(Context& c);
+
+}  // namespace cfd

@@ -1,0 +1,224 @@
+// Internal declarations of the chebfd_b200 library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/chebfd_b200.h"
+
+struct cublasContext;
+struct cusolverDnContext;
+typedef struct ncclComm* ncclComm_t;
+
+namespace cfd {
+
+// ---- errors: internal C++ exceptions mapped to status codes at the ABI --------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool ok, const std::string& msg) {
+    if (!ok) fail(CHEBFD_ERR_INVALID_ARGUMENT, msg);
+}
+void cuda_check(cudaError_t e, const char* what);
+#define CFD_CUDA(x) ::cfd::cuda_check((x), #x)
+
+// ---- device memory --------------------------------------------------------------
+struct DeviceBuffer {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(size_t n);
+    ~DeviceBuffer();
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    void ensure(size_t n);  // grow-only
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- row partition of a distributed operator ---------------------------------------
+// Rows [row_begin, row_begin+local) are owned.  Gathered operands live in an
+// extended row space [halo_lo | owned | halo_hi]; halo_lo holds the global
+// rows [lo_src_begin, lo_src_begin+halo_lo) owned by rank lo_rank, halo_hi
+// the rows [hi_src_begin, ...) owned by hi_rank.
+struct Partition {
+    int64_t dim = 0;  // global
+    int64_t row_begin = 0, local = 0;
+    int64_t halo_lo = 0, halo_hi = 0;
+    int64_t lo_src_begin = 0, hi_src_begin = 0;
+    int lo_rank = -1, hi_rank = -1;
+    // rows that read the halo: [0, bnd_lo) and [local - bnd_hi, local)
+    int64_t bnd_lo = 0, bnd_hi = 0;
+    // neighbours' requests of our rows: we send rows [send_lo_begin, +send_lo_n)
+    // (local index) to lo_rank and [send_hi_begin, +send_hi_n) to hi_rank
+    int64_t send_lo_begin = 0, send_lo_n = 0, send_hi_begin = 0, send_hi_n = 0;
+    int64_t ext_rows() const { return halo_lo + local + halo_hi; }
+};
+
+struct Context;
+
+// ---- SELL-C-sigma matrix (C = 32, sigma = 1) ---------------------------------------
+constexpr int kChunk = 32;
+
+struct Matrix {
+    Context* ctx = nullptr;
+    int kind = 0;
+    int64_t nnz_global = 0, nnz_local = 0;
+    int max_row_len = 0;
+    Partition part;
+    int64_t nchunks = 0;
+    int64_t entries = 0;     // SELL slots (padding included)
+    DeviceBuffer chunk_ptr;  // int64[nchunks+1], slot offsets
+    DeviceBuffer cols;       // int32[entries], extended-row index or -1 padding
+    DeviceBuffer vals;       // double or double2 [entries]
+};
+
+// ---- block vector -------------------------------------------------------------------
+struct Block {
+    Context* ctx = nullptr;
+    int kind = 0;
+    int64_t rows = 0;   // owned rows
+    int64_t width = 0;
+    int64_t halo_lo = 0, halo_hi = 0;  // extra rows (gather halos)
+    int64_t row_begin = 0, dim_global = 0;
+    const Matrix* shape_of = nullptr;  // partition the halos belong to (may be null)
+    DeviceBuffer buf;   // (halo_lo + rows + halo_hi) x width scalars
+    size_t scalar_bytes() const { return kind ? 16 : 8; }
+    void* base() const { return buf.p; }  // extended row 0
+    void* owned() const {
+        return static_cast<char*>(buf.p) + halo_lo * width * scalar_bytes();
+    }
+    size_t owned_bytes() const { return static_cast<size_t>(rows * width) * scalar_bytes(); }
+};
+
+// ---- context -----------------------------------------------------------------------
+struct GraphKey {
+    const void* a;
+    const void* x;
+    int degree;
+    uint64_t alpha_bits, beta_bits;
+    bool moments;
+    int64_t width;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(a, x, degree, alpha_bits, beta_bits, moments, width) <
+               std::tie(o.a, o.x, o.degree, o.alpha_bits, o.beta_bits, o.moments, o.width);
+    }
+};
+
+struct DeviceBuffer;
+// A captured apply_filter: the graph reads its coefficients from `coeff`
+// (refreshed before every replay) and writes moments into `moments`.
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    std::shared_ptr<DeviceBuffer> coeff, moments;
+    int64_t kernels = 0;
+};
+
+struct FilterWorkspace {
+    std::unique_ptr<Block> u, w, x0;
+};
+
+struct Context {
+    int device = 0, rank = 0, nranks = 1, num_sms = 148;
+    cudaStream_t stream = nullptr;       // compute
+    cudaStream_t comm_stream = nullptr;  // halo exchange
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    cudaEvent_t timers[16] = {};
+    cublasContext* cublas = nullptr;
+    cusolverDnContext* cusolver = nullptr;
+    ncclComm_t nccl = nullptr;
+    bool use_graphs = true, overlap = true;
+    int64_t launches = 0;
+    // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
+    DeviceBuffer partials;   // per-block partial sums
+    DeviceBuffer counter;    // last-block-done ticket (uint32), self-resetting
+    DeviceBuffer dscratch;   // small device results (dots, Gram, moments)
+    DeviceBuffer workspace;  // cuSOLVER / misc
+    DeviceBuffer devinfo;
+    DeviceBuffer coeffs;     // filter coefficients (device copy)
+    void* host_pinned = nullptr;  // small pinned staging
+    size_t host_pinned_bytes = 0;
+    std::map<GraphKey, GraphEntry> graphs;
+    std::map<std::tuple<const void*, int64_t, int>, FilterWorkspace> filter_ws;
+    ~Context();
+    void* pinned(size_t bytes);
+};
+
+// ---- launchers (kernels.cu) ------------------------------------------------------------
+enum StepKind {
+    kStepSpmmvm = 0,   // Y = (alpha A + beta I) X, beta added iff != 0
+    kStepStart2 = 1,   // startup step 2 of apply_filter (filter.hpp:93-103)
+    kStepFused = 2,    // spmmvm_fused (kernels.hpp:74-118)
+    kStepRecur = 3,    // recurrence_step (kernels.hpp:121-145)
+};
+
+struct StepArgs {
+    int kind_step;
+    const Matrix* a;
+    int64_t width_cols;      // block width in columns
+    int64_t row0, row1;      // owned-row range processed by this launch
+    const void* in;          // gathered operand, extended-row base
+    void* w;                 // W (in/out) or Y (out); owned base
+    void* x;                 // X (in/out) owned base, or null
+    void* x0;                // x0 for moments (read; written in kStepSpmmvm copy mode)
+    double alpha, beta;      // (2alpha, 2beta) already doubled for fused/recur/start2
+    double c0, c1, c2;       // start2 combination / fused coeff in c0
+    const double* coeff_dev; // fused: device coefficient array (graph-friendly) or null
+    int coeff_index;
+    int dots_mode;           // 0 none, 1 <x_old, w> (Kahan, complex), 2 Re<x0, w>, 3 m0+m1 (spmmvm start)
+    void* dots_out;          // device output (S[nb] for mode 1, double[nb] for 2, 2*nb for 3)
+    int partial_base;        // first partial slot of this launch
+    bool final_launch;       // this launch reduces all partials [0, partial_base + grid)
+    int* grid_used;          // out: number of blocks used
+};
+void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st);
+
+void launch_axpy(Context& ctx, Block& x, const Block& u, const Block& w, double c0, double c1,
+                 double c2, cudaStream_t st);
+// out[k] = sum_i f(x_ik, y_ik) over owned rows; mode 0: conj(x) y (S), 1: |x|^2 (double)
+void launch_column_reduce(Context& ctx, const Block& x, const Block& y, int mode, void* dev_out,
+                          cudaStream_t st);
+// out[k] = || av_k - lambda_k v_k ||^2 (double)
+void launch_residual_sq(Context& ctx, const Block& av, const Block& v, const double* lambda_dev,
+                        void* dev_out, cudaStream_t st);
+// x(:,k) /= d[k] (d on the device)
+void launch_scale_columns(Context& ctx, Block& b, const double* d_dev, cudaStream_t st);
+// w <- w - h q (single column, h real or complex)
+void launch_axpy_scalar(Context& ctx, Block& w, const Block& q, double hr, double hi,
+                        cudaStream_t st);
+void launch_copy_columns(Context& ctx, Block& dst, int64_t d0, const Block& src, int64_t s0,
+                         int64_t n, cudaStream_t st);
+void launch_philox_normal(Context& ctx, Block& b, uint64_t seed, cudaStream_t st);
+// SELL build from a device CSR (global column indices -> extended-row index)
+void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d_cols,
+                const void* d_vals, cudaStream_t st);
+
+// ---- host helpers (host.cpp) --------------------------------------------------------------
+struct HostCsr {
+    int kind = 0;
+    int64_t dim = 0, row_begin = 0, rows = 0;
+    std::vector<int64_t> offs, cols;  // offs relative to row_begin
+    std::vector<double> vals;         // interleaved for complex
+};
+HostCsr gen_graphene(const chebfd_lattice& s, int64_t r0, int64_t r1);
+HostCsr gen_topological_insulator(const chebfd_lattice& s, int64_t r0, int64_t r1);
+void validate_lattice(const chebfd_lattice& s, bool needs_z);
+// std::mt19937_64 + std::normal_distribution stream (block_vector.hpp:42-51):
+// entries [first, first+count) of the row-major global block
+void host_randomize(int kind, uint64_t seed, int64_t first, int64_t count, void* out);
+std::vector<double> window_coeffs(double tlo, double thi, double blo, double bhi, int degree);
+std::vector<double> kernel_coeffs(int kind, int mu, int degree);
+double dos_count(const double* mu, int order, double blo, double bhi, double lo, double hi);
+// plane partition of `dim` rows into nranks parts, boundaries on multiples of `plane`
+void plane_partition(int64_t dim, int64_t plane, int rank, int nranks, int64_t* r0, int64_t* r1);
+
+}  // namespace cfd

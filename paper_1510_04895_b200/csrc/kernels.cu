@@ -1,0 +1,789 @@
+// Device kernels of the ChebFD hot path (sm_100a).
+//
+// Design:
+//  * SELL-C-sigma matrix, C = 32, sigma = 1 (row order kept): entry j of row
+//    r lives at chunk_ptr[r/32] + j*32 + r%32, int32 extended-row column
+//    index (-1 = padding), value double / double2.
+//  * Row-major block vectors.  One THREAD owns one 16-byte unit of a row
+//    (one complex entry, or two real columns; 8 bytes for odd real widths);
+//    a CTA covers R consecutive rows x U units, so the own-row streams
+//    (W, X, x0) are perfectly coalesced and every gathered neighbour row is a
+//    contiguous, fully used segment.
+//  * Persistent grid (num_SMs x occupancy), rows strided by the grid.
+//  * Column dot products: per-thread accumulators -> fixed-order CTA reduction
+//    -> per-CTA partials -> the last CTA (ticket counter) reduces the partials
+//    in CTA order.  Bitwise run-to-run reproducible.
+//  * Arithmetic uses __dmul_rn/__dadd_rn/__dsub_rn in exactly the order of the
+//    reference's scalar code (kernels.hpp:46-118 compiled for x86-64 SSE2, no
+//    FMA), so W and X match the reference bit for bit; only the dot-product
+//    summation order differs (tolerance-checked).
+#include <cuda_runtime.h>
+#include <curand_kernel.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include "internal.hpp"
+
+namespace cfd {
+
+namespace {
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
+
+template <class T>
+__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// Streaming loads/stores (evict-first) for the read-once / write-once streams.
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+
+// ---- scalar traits: (complex?, unit type) ------------------------------------------
+template <bool CPLX, class T>
+struct Ops;
+
+// real, one column per unit
+template <>
+struct Ops<false, double> {
+    using M = double;
+    static constexpr int kCols = 1;
+    __device__ static double zero() { return 0.0; }
+    __device__ static M scale(M a, double s) { return mul(a, s); }
+    __device__ static double prod(M a, double u) { return mul(a, u); }
+    __device__ static double vadd(double a, double b) { return add(a, b); }
+    __device__ static double vsub(double a, double b) { return sub(a, b); }
+    __device__ static double smul(double s, double v) { return mul(s, v); }
+    __device__ static double cdot(double x, double w) { return mul(x, w); }
+    __device__ static double lam_mul(const double* lam, int col, double v) { return mul(lam[col], v); }
+    __device__ static double cdiv(double v, const double* d, int col) { return div_(v, d[col]); }
+    __device__ static void store_re(double* out, int unit, double v) { out[unit] = v; }
+    __device__ static void store_full(double* out, int unit, double v) { out[unit] = v; }
+};
+
+// real, two columns per unit
+template <>
+struct Ops<false, double2> {
+    using M = double;
+    static constexpr int kCols = 2;
+    __device__ static double2 zero() { return make_double2(0.0, 0.0); }
+    __device__ static M scale(M a, double s) { return mul(a, s); }
+    __device__ static double2 prod(M a, double2 u) { return make_double2(mul(a, u.x), mul(a, u.y)); }
+    __device__ static double2 vadd(double2 a, double2 b) { return make_double2(add(a.x, b.x), add(a.y, b.y)); }
+    __device__ static double2 vsub(double2 a, double2 b) { return make_double2(sub(a.x, b.x), sub(a.y, b.y)); }
+    __device__ static double2 smul(double s, double2 v) { return make_double2(mul(s, v.x), mul(s, v.y)); }
+    __device__ static double2 cdot(double2 x, double2 w) { return make_double2(mul(x.x, w.x), mul(x.y, w.y)); }
+    __device__ static double2 lam_mul(const double* lam, int col, double2 v) {
+        return make_double2(mul(lam[col], v.x), mul(lam[col + 1], v.y));
+    }
+    __device__ static double2 cdiv(double2 v, const double* d, int col) {
+        return make_double2(div_(v.x, d[col]), div_(v.y, d[col + 1]));
+    }
+    __device__ static void store_re(double* out, int unit, double2 v) {
+        out[2 * unit] = v.x;
+        out[2 * unit + 1] = v.y;
+    }
+    __device__ static void store_full(double2* out, int unit, double2 v) { out[unit] = v; }
+};
+
+// complex, one column per unit (std::complex<double> layout)
+template <>
+struct Ops<true, double2> {
+    using M = double2;
+    static constexpr int kCols = 1;
+    __device__ static double2 zero() { return make_double2(0.0, 0.0); }
+    // complex * double (libstdc++ operator*(complex, T): componentwise)
+    __device__ static M scale(M a, double s) { return make_double2(mul(a.x, s), mul(a.y, s)); }
+    // complex * complex, GCC inline expansion: (ac - bd, ad + bc)
+    __device__ static double2 prod(M a, double2 u) {
+        return make_double2(sub(mul(a.x, u.x), mul(a.y, u.y)), add(mul(a.x, u.y), mul(a.y, u.x)));
+    }
+    __device__ static double2 vadd(double2 a, double2 b) { return make_double2(add(a.x, b.x), add(a.y, b.y)); }
+    __device__ static double2 vsub(double2 a, double2 b) { return make_double2(sub(a.x, b.x), sub(a.y, b.y)); }
+    __device__ static double2 smul(double s, double2 v) { return make_double2(mul(s, v.x), mul(s, v.y)); }
+    // conj(x) * w
+    __device__ static double2 cdot(double2 x, double2 w) {
+        const double nxi = -x.y;
+        return make_double2(sub(mul(x.x, w.x), mul(nxi, w.y)), add(mul(x.x, w.y), mul(nxi, w.x)));
+    }
+    __device__ static double2 lam_mul(const double* lam, int col, double2 v) { return smul(lam[col], v); }
+    __device__ static double2 cdiv(double2 v, const double* d, int col) {
+        return make_double2(div_(v.x, d[col]), div_(v.y, d[col]));
+    }
+    __device__ static void store_re(double* out, int unit, double2 v) { out[unit] = v.x; }
+    __device__ static void store_full(double2* out, int unit, double2 v) { out[unit] = v; }
+};
+
+template <class T>
+__device__ __forceinline__ void kahan_add(T& s, T& c, T v);
+template <>
+__device__ __forceinline__ void kahan_add<double>(double& s, double& c, double v) {
+    const double y = sub(v, c);
+    const double t = add(s, y);
+    c = sub(sub(t, s), y);
+    s = t;
+}
+template <>
+__device__ __forceinline__ void kahan_add<double2>(double2& s, double2& c, double2 v) {
+    kahan_add<double>(s.x, c.x, v.x);
+    kahan_add<double>(s.y, c.y, v.y);
+}
+
+template <class T>
+__device__ __forceinline__ T tadd(T a, T b);
+template <>
+__device__ __forceinline__ double tadd<double>(double a, double b) { return add(a, b); }
+template <>
+__device__ __forceinline__ double2 tadd<double2>(double2 a, double2 b) {
+    return make_double2(add(a.x, b.x), add(a.y, b.y));
+}
+
+// ---- fixed-order block + grid reduction of NDOT per-unit accumulators -------------
+// Threads are laid out t = rr*US + u.  Each CTA writes NDOT*US partials; the
+// last CTA to finish (ticket) sums partial rows [0, nparts) in order and
+// hands the totals to `emit(d, u, value)`.
+template <class T, int NDOT, class Emit>
+__device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1], int R, int US,
+                                            T* partials, int part_slot, int nparts, bool final_launch,
+                                            unsigned* counter, Emit emit) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sred = reinterpret_cast<T*>(smem_raw);
+    const int t = threadIdx.x;
+    const int rr = t / US, u = t - rr * US;
+    const int nthr = R * US;
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) sred[d * nthr + t] = acc[d];
+    __syncthreads();
+    if (rr == 0) {
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) {
+            T s = sred[d * nthr + u];
+            for (int q = 1; q < R; ++q) s = tadd(s, sred[d * nthr + q * US + u]);
+            partials[(static_cast<int64_t>(part_slot) * NDOT + d) * US + u] = s;
+        }
+    }
+    if (!final_launch) return;
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned is_last;
+    if (t == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) {
+        T s = T{};
+        bool first = true;
+        for (int q = rr; q < nparts; q += R) {
+            const T v = __ldcg(&partials[(static_cast<int64_t>(q) * NDOT + d) * US + u]);
+            s = first ? v : tadd(s, v);
+            first = false;
+        }
+        if (first) s = T{};
+        sred[d * nthr + t] = s;
+    }
+    __syncthreads();
+    if (rr == 0) {
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) {
+            T s = sred[d * nthr + u];
+            const int lim = R < nparts ? R : nparts;
+            for (int q = 1; q < lim; ++q) s = tadd(s, sred[d * nthr + q * US + u]);
+            emit(d, u, s);
+        }
+    }
+    if (t == 0) *counter = 0u;  // self-reset for the next stream-ordered launch
+}
+
+// ---- the Chebyshev step kernel --------------------------------------------------------
+struct StepParams {
+    const int64_t* chunk_ptr;
+    const int* cols;
+    const void* vals;
+    int64_t row0, row1;   // owned rows of this launch
+    int64_t halo_lo;      // extended-row offset of owned row 0
+    int pitch;            // units per row in memory
+    int u_off;            // first unit of this column slab
+    int US;               // units in this slab (threads per row)
+    int R;                // rows per CTA iteration
+    const void* in;       // gathered operand (extended base)
+    void* w;              // owned base
+    void* x;
+    void* x0;
+    double alpha, beta;   // already 2x for start2/fused/recur
+    double c0, c1, c2;
+    const double* coeff_dev;
+    int coeff_index;
+    void* dots_out;
+    int64_t dots_row_stride;  // doubles between the NDOT output rows (moment rows)
+    void* partials;
+    int part_base;
+    int nparts;
+    int final_launch;
+    unsigned* counter;
+};
+
+template <bool CPLX, class T, int KIND, int DMODE>
+__global__ void __launch_bounds__(256) step_kernel(const StepParams p) {
+    using O = Ops<CPLX, T>;
+    using M = typename O::M;
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr int BATCH = 4;
+    const int t = threadIdx.x;
+    const int rr = t / p.US;
+    const int u = t - rr * p.US;
+    const int R = p.R;
+    const T* __restrict__ in = static_cast<const T*>(p.in);
+    T* __restrict__ W = static_cast<T*>(p.w);
+    T* __restrict__ X = static_cast<T*>(p.x);
+    T* __restrict__ X0 = static_cast<T*>(p.x0);
+    const M* __restrict__ vals = static_cast<const M*>(p.vals);
+    const int* __restrict__ cols = p.cols;
+    double coeff = p.c0, c1 = p.c1, c2 = p.c2;
+    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepStart2 && p.coeff_dev) {
+        coeff = p.coeff_dev[0];
+        c1 = p.coeff_dev[1];
+        c2 = p.coeff_dev[2];
+    }
+
+    T acc_d[NDOT > 0 ? NDOT : 1];
+    T comp_d[NDOT > 0 ? NDOT : 1];
+#pragma unroll
+    for (int d = 0; d < (NDOT > 0 ? NDOT : 1); ++d) {
+        acc_d[d] = O::zero();
+        comp_d[d] = O::zero();
+    }
+
+    const int64_t nrows = p.row1 - p.row0;
+    const int64_t col_off = p.u_off + u;
+    for (int64_t rg = blockIdx.x; rg * R < nrows; rg += gridDim.x) {
+        const int64_t rl = rg * R + rr;
+        if (rl >= nrows) continue;
+        const int64_t r = p.row0 + rl;  // owned row
+        const int64_t chunk = r >> 5;
+        const int lane = static_cast<int>(r & 31);
+        const int64_t base = __ldg(&p.chunk_ptr[chunk]);
+        const int width = static_cast<int>((__ldg(&p.chunk_ptr[chunk + 1]) - base) >> 5);
+        T acc = O::zero();
+        for (int j0 = 0; j0 < width; j0 += BATCH) {
+            int c[BATCH];
+            M v[BATCH];
+            T g[BATCH];
+#pragma unroll
+            for (int b = 0; b < BATCH; ++b) {
+                c[b] = -1;
+                if (j0 + b < width) {
+                    const int64_t idx = base + static_cast<int64_t>(j0 + b) * 32 + lane;
+                    c[b] = __ldg(&cols[idx]);
+                    v[b] = __ldg(&vals[idx]);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < BATCH; ++b)
+                if (c[b] >= 0) g[b] = ldg(&in[static_cast<int64_t>(c[b]) * p.pitch + col_off]);
+#pragma unroll
+            for (int b = 0; b < BATCH; ++b)
+                if (c[b] >= 0) acc = O::vadd(acc, O::prod(O::scale(v[b], p.alpha), g[b]));
+        }
+        const int64_t own = r * p.pitch + col_off;
+        const T ui = ldg(&in[(r + p.halo_lo) * p.pitch + col_off]);
+        if constexpr (KIND == kStepSpmmvm) {
+            T y = acc;
+            if (p.beta != 0.0) y = O::vadd(y, O::smul(p.beta, ui));
+            st_stream(&W[own], y);
+            if constexpr (DMODE == 3) {  // apply_filter entry: x0 = X, m0 = <x,x>, m1 = <x,u>
+                st_stream(&X0[own], ui);
+                acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, ui));
+                acc_d[1] = O::vadd(acc_d[1], O::cdot(ui, y));
+            }
+        } else if constexpr (KIND == kStepStart2) {
+            // w = spmmvm(A,u,2a,2b); w = 1*w + (-1)*x + 0*x; x = c0 x + c1 u + c2 w
+            T wr = acc;
+            if (p.beta != 0.0) wr = O::vadd(wr, O::smul(p.beta, ui));
+            const T xi = ld_stream(&X[own]);
+            const T wn = O::vadd(O::vadd(O::smul(1.0, wr), O::smul(-1.0, xi)), O::smul(0.0, xi));
+            st_stream(&W[own], wn);
+            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(xi, wn));
+            const T xn = O::vadd(O::vadd(O::smul(coeff, xi), O::smul(c1, ui)), O::smul(c2, wn));
+            st_stream(&X[own], xn);
+        } else {
+            // fused / recur: w' = tmp + 2b u_i - w_i
+            const T wi = ld_stream(&W[own]);
+            const T wn = O::vsub(O::vadd(acc, O::smul(p.beta, ui)), wi);
+            st_stream(&W[own], wn);
+            if constexpr (KIND == kStepFused) {
+                const T xi = ld_stream(&X[own]);
+                if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
+                if constexpr (DMODE == 2) {
+                    const T x0 = ld_stream(&X0[own]);
+                    acc_d[0] = O::vadd(acc_d[0], O::cdot(x0, wn));
+                }
+                st_stream(&X[own], O::vadd(xi, O::smul(coeff, wn)));
+            } else {
+                if constexpr (DMODE == 2) {
+                    const T x0 = ld_stream(&X0[own]);
+                    acc_d[0] = O::vadd(acc_d[0], O::cdot(x0, wn));
+                }
+            }
+        }
+    }
+
+    if constexpr (NDOT > 0) {
+        T acc_out[NDOT];
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) acc_out[d] = acc_d[d];
+        const int US = p.US;
+        const int uoff = p.u_off;
+        void* outp = p.dots_out;
+        const int64_t stride = p.dots_row_stride;
+        grid_reduce<T, NDOT>(acc_out, R, US, static_cast<T*>(p.partials), p.part_base + blockIdx.x,
+                             p.nparts, p.final_launch != 0, p.counter,
+                             [&](int d, int uu, T v) {
+                                 if (DMODE == 1)
+                                     O::store_full(static_cast<T*>(outp), uoff + uu, v);
+                                 else
+                                     O::store_re(static_cast<double*>(outp) + d * stride,
+                                                 uoff + uu, v);
+                             });
+    }
+}
+
+// ---- generic per-column reductions ------------------------------------------------------
+// mode 0: out_S[k] = sum conj(x) y;  mode 1: out_d[k] = sum |av - lam v|^2
+template <bool CPLX, class T, int MODE>
+__global__ void __launch_bounds__(256) colreduce_kernel(const T* __restrict__ x,
+                                                        const T* __restrict__ y,
+                                                        const double* __restrict__ lam,
+                                                        int64_t rows, int pitch, int u_off,
+                                                        int US, int R, void* out, T* partials,
+                                                        unsigned* counter) {
+    using O = Ops<CPLX, T>;
+    const int t = threadIdx.x;
+    const int rr = t / US, u = t - rr * US;
+    const int64_t col = u_off + u;
+    T acc[1] = {O::zero()};
+    for (int64_t rg = blockIdx.x; rg * R < rows; rg += gridDim.x) {
+        const int64_t r = rg * R + rr;
+        if (r >= rows) continue;
+        const T a = ld_stream(&x[r * pitch + col]);
+        const T b = ld_stream(&y[r * pitch + col]);
+        if constexpr (MODE == 0) {
+            acc[0] = O::vadd(acc[0], O::cdot(a, b));
+        } else {
+            const T res = O::vsub(a, O::lam_mul(lam, static_cast<int>(col) * O::kCols, b));
+            acc[0] = O::vadd(acc[0], O::cdot(res, res));
+        }
+    }
+    grid_reduce<T, 1>(acc, R, US, partials, blockIdx.x, gridDim.x, true, counter,
+                      [&](int, int uu, T v) {
+                          if (MODE == 0)
+                              O::store_full(static_cast<T*>(out), u_off + uu, v);
+                          else
+                              O::store_re(static_cast<double*>(out), u_off + uu, v);
+                      });
+}
+
+// X = c0 X + c1 U + c2 W on flat doubles (block_axpy_scal, kernels.hpp:147-162)
+__global__ void axpy_kernel(double* __restrict__ x, const double* __restrict__ u,
+                            const double* __restrict__ w, int64_t n, double c0, double c1,
+                            double c2) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] = add(add(mul(c0, x[i]), mul(c1, u[i])), mul(c2, w[i]));
+}
+
+// w <- w - h q for single-column blocks (Lanczos reorthogonalisation,
+// spectral.cpp:119): real h*q, or GCC's complex expansion of h*q.
+__global__ void axpy_scalar_kernel(double* __restrict__ w, const double* __restrict__ q, int64_t n,
+                                   int cplx, double hr, double hi) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (!cplx) {
+            w[i] = sub(w[i], mul(hr, q[i]));
+        } else {
+            const double qr = q[2 * i], qi = q[2 * i + 1];
+            const double pr = sub(mul(hr, qr), mul(hi, qi));
+            const double pi = add(mul(hr, qi), mul(hi, qr));
+            w[2 * i] = sub(w[2 * i], pr);
+            w[2 * i + 1] = sub(w[2 * i + 1], pi);
+        }
+    }
+}
+
+// x(i,k) /= d[k] on doubles: complex entries divide both parts by d[k]
+__global__ void divcols_kernel(double* __restrict__ x, int64_t rows, int64_t width, int cplx,
+                               const double* __restrict__ d) {
+    const int64_t per_row = width * (cplx ? 2 : 1);
+    const int64_t n = rows * per_row;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k = (i % per_row) >> cplx;
+        x[i] = div_(x[i], d[k]);
+    }
+}
+
+__global__ void copycols_kernel(double* __restrict__ dst, int64_t dpitch, int64_t d0,
+                                const double* __restrict__ src, int64_t spitch, int64_t s0,
+                                int64_t rows, int64_t n) {
+    const int64_t tot = rows * n;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / n, k = i - r * n;
+        dst[r * dpitch + d0 + k] = src[r * spitch + s0 + k];
+    }
+}
+
+__global__ void philox_normal_kernel(double* __restrict__ x, int64_t n, uint64_t seed) {
+    const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    curandStatePhilox4_32_10_t st;
+    curand_init(seed, tid, 0, &st);
+    for (int64_t i = 2 * tid; i < n; i += 2 * static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double2 g = curand_normal2_double(&st);
+        x[i] = g.x;
+        if (i + 1 < n) x[i + 1] = g.y;
+    }
+}
+
+// ---- SELL build --------------------------------------------------------------------------
+__global__ void sell_width_kernel(const int64_t* __restrict__ offs, int64_t rows, int64_t nchunks,
+                                  int64_t* __restrict__ slots, int* __restrict__ maxlen) {
+    const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (c >= nchunks) return;
+    int64_t w = 0;
+    for (int l = 0; l < kChunk; ++l) {
+        const int64_t r = c * kChunk + l;
+        if (r < rows) w = max(w, offs[r + 1] - offs[r]);
+    }
+    slots[c] = w * kChunk;
+    atomicMax(maxlen, static_cast<int>(w));
+}
+
+struct ColMap {
+    int64_t row_begin, local, halo_lo, halo_hi, lo_src, hi_src;
+    __device__ int map(int64_t g) const {
+        if (g >= row_begin && g < row_begin + local) return static_cast<int>(g - row_begin + halo_lo);
+        if (g >= lo_src && g < lo_src + halo_lo) return static_cast<int>(g - lo_src);
+        if (g >= hi_src && g < hi_src + halo_hi) return static_cast<int>(g - hi_src + halo_lo + local);
+        return -2;  // not representable: error
+    }
+};
+
+template <class M>
+__global__ void sell_fill_kernel(const int64_t* __restrict__ offs, const int64_t* __restrict__ gcols,
+                                 const M* __restrict__ gvals, int64_t rows,
+                                 const int64_t* __restrict__ chunk_ptr, int* __restrict__ cols,
+                                 M* __restrict__ vals, ColMap cm, int* __restrict__ err) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t nch = (rows + kChunk - 1) / kChunk;
+    if (r >= nch * kChunk) return;
+    const int64_t chunk = r / kChunk;
+    const int lane = static_cast<int>(r % kChunk);
+    const int64_t base = chunk_ptr[chunk];
+    const int64_t width = (chunk_ptr[chunk + 1] - base) / kChunk;
+    const int64_t b = r < rows ? offs[r] : 0, e = r < rows ? offs[r + 1] : 0;
+    for (int64_t j = 0; j < width; ++j) {
+        const int64_t slot = base + j * kChunk + lane;
+        if (b + j < e) {
+            const int c = cm.map(gcols[b + j]);
+            if (c < 0) atomicExch(err, 1);
+            cols[slot] = c;
+            vals[slot] = gvals[b + j];
+        } else {
+            cols[slot] = -1;
+            vals[slot] = M{};
+        }
+    }
+}
+
+// ---- launch geometry -----------------------------------------------------------------------
+struct Geometry {
+    int US;      // units per row in this slab
+    int R;       // rows per CTA iteration
+    int threads;
+};
+
+inline Geometry geometry(int units) {
+    Geometry g;
+    g.US = units;
+    g.R = units >= 256 ? 1 : 256 / units;
+    g.threads = g.R * g.US;
+    return g;
+}
+
+template <class K>
+int max_blocks_for(K kernel, int threads, size_t smem, int num_sms) {
+    int per_sm = 0;
+    CFD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    return std::max(1, per_sm) * num_sms;
+}
+
+template <bool CPLX, class T, int KIND, int DMODE>
+void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
+    const Matrix& a = *s.a;
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    const int64_t nrows = s.row1 - s.row0;
+    auto kernel = step_kernel<CPLX, T, KIND, DMODE>;
+    int used_total = 0;
+    // column slabs of at most 256 units (one CTA row-group spans a slab)
+    for (int u0 = 0; u0 < units; u0 += 256) {
+        const int us = std::min(256, units - u0);
+        Geometry g = geometry(us);
+        const size_t smem = NDOT * static_cast<size_t>(g.threads) * sizeof(T);
+        static thread_local std::map<std::pair<const void*, int>, int> occ_cache;
+        auto key = std::make_pair(reinterpret_cast<const void*>(kernel), g.threads);
+        auto it = occ_cache.find(key);
+        int maxb = 0;
+        if (it == occ_cache.end()) {
+            maxb = max_blocks_for(kernel, g.threads, smem, ctx.num_sms);
+            occ_cache[key] = maxb;
+        } else {
+            maxb = it->second;
+        }
+        const int64_t need = (nrows + g.R - 1) / g.R;
+        const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, maxb)));
+        StepParams p{};
+        p.chunk_ptr = a.chunk_ptr.as<int64_t>();
+        p.cols = a.cols.as<int>();
+        p.vals = a.vals.p;
+        p.row0 = s.row0;
+        p.row1 = s.row1;
+        p.halo_lo = a.part.halo_lo;
+        p.pitch = pitch;
+        p.u_off = u0;
+        p.US = us;
+        p.R = g.R;
+        p.in = s.in;
+        p.w = s.w;
+        p.x = s.x;
+        p.x0 = s.x0;
+        p.alpha = s.alpha;
+        p.beta = s.beta;
+        p.c0 = s.c0;
+        p.c1 = s.c1;
+        p.c2 = s.c2;
+        p.coeff_dev = s.coeff_dev;
+        p.coeff_index = s.coeff_index;
+        p.dots_out = s.dots_out;
+        p.dots_row_stride = static_cast<int64_t>(units) * Ops<CPLX, T>::kCols;  // = nb columns
+        if (NDOT > 0) {
+            const size_t need_bytes =
+                static_cast<size_t>(s.partial_base + grid) * NDOT * us * sizeof(T);
+            // partials are slab-local: slabs run sequentially on the stream
+            ctx.partials.ensure(std::max<size_t>(need_bytes, 1 << 20));
+            ctx.counter.ensure(256);
+        }
+        p.partials = ctx.partials.p;
+        p.part_base = s.partial_base;
+        p.nparts = s.partial_base + grid;
+        p.final_launch = s.final_launch ? 1 : 0;
+        p.counter = ctx.counter.as<unsigned>();
+        if (nrows > 0) {
+            kernel<<<grid, g.threads, smem, st>>>(p);
+            CFD_CUDA(cudaGetLastError());
+            ctx.launches++;
+        }
+        used_total = grid;
+        if (units > 256 && NDOT > 0 && !s.final_launch)
+            fail(CHEBFD_ERR_UNSUPPORTED, "split dot launches need width <= 256 units");
+    }
+    if (s.grid_used) *s.grid_used = used_total;
+}
+
+template <bool CPLX, class T>
+void dispatch_kind(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
+    switch (s.kind_step) {
+        case kStepSpmmvm:
+            if (s.dots_mode == 3) return run_step<CPLX, T, kStepSpmmvm, 3>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepSpmmvm, 0>(ctx, s, st, units, pitch);
+        case kStepStart2:
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepStart2, 2>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepStart2, 0>(ctx, s, st, units, pitch);
+        case kStepFused:
+            if (s.dots_mode == 1) return run_step<CPLX, T, kStepFused, 1>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepFused, 2>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepFused, 0>(ctx, s, st, units, pitch);
+        case kStepRecur:
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepRecur, 2>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepRecur, 0>(ctx, s, st, units, pitch);
+    }
+    fail(CHEBFD_ERR_INVALID_ARGUMENT, "bad step kind");
+}
+
+}  // namespace
+
+// width (columns) -> units per row / unit type
+void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st) {
+    const int kind = s.a->kind;
+    const int64_t width = s.width_cols;
+    if (kind == CHEBFD_COMPLEX128) {
+        dispatch_kind<true, double2>(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
+    } else if (width % 2 == 0) {
+        dispatch_kind<false, double2>(ctx, s, st, static_cast<int>(width / 2),
+                                      static_cast<int>(width / 2));
+    } else {
+        dispatch_kind<false, double>(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
+    }
+}
+
+void launch_axpy(Context& ctx, Block& x, const Block& u, const Block& w, double c0, double c1,
+                 double c2, cudaStream_t st) {
+    const int64_t n = x.rows * x.width * (x.kind ? 2 : 1);
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, ctx.num_sms * 8));
+    axpy_kernel<<<grid, 256, 0, st>>>(static_cast<double*>(x.owned()),
+                                      static_cast<const double*>(u.owned()),
+                                      static_cast<const double*>(w.owned()), n, c0, c1, c2);
+    CFD_CUDA(cudaGetLastError());
+    ctx.launches++;
+}
+
+namespace {
+template <bool CPLX, class T, int MODE>
+void run_colreduce(Context& ctx, const Block& x, const Block& y, const double* lam, void* out,
+                   cudaStream_t st, int units) {
+    auto kernel = colreduce_kernel<CPLX, T, MODE>;
+    for (int u0 = 0; u0 < units; u0 += 256) {
+        const int us = std::min(256, units - u0);
+        Geometry g = geometry(us);
+        const size_t smem = static_cast<size_t>(g.threads) * sizeof(T);
+        const int maxb = max_blocks_for(kernel, g.threads, smem, ctx.num_sms);
+        const int64_t need = (x.rows + g.R - 1) / g.R;
+        const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, maxb)));
+        ctx.partials.ensure(std::max<size_t>(static_cast<size_t>(grid) * us * sizeof(T), 1 << 20));
+        ctx.counter.ensure(256);
+        kernel<<<grid, g.threads, smem, st>>>(
+            static_cast<const T*>(x.owned()), static_cast<const T*>(y.owned()), lam, x.rows,
+            units, u0, us, g.R, out, ctx.partials.as<T>(), ctx.counter.as<unsigned>());
+        CFD_CUDA(cudaGetLastError());
+        ctx.launches++;
+    }
+}
+}  // namespace
+
+void launch_column_reduce(Context& ctx, const Block& x, const Block& y, int mode, void* dev_out,
+                          cudaStream_t st) {
+    (void)mode;
+    if (x.kind == CHEBFD_COMPLEX128)
+        run_colreduce<true, double2, 0>(ctx, x, y, nullptr, dev_out, st, static_cast<int>(x.width));
+    else if (x.width % 2 == 0)
+        run_colreduce<false, double2, 0>(ctx, x, y, nullptr, dev_out, st, static_cast<int>(x.width / 2));
+    else
+        run_colreduce<false, double, 0>(ctx, x, y, nullptr, dev_out, st, static_cast<int>(x.width));
+}
+
+void launch_residual_sq(Context& ctx, const Block& av, const Block& v, const double* lam,
+                        void* dev_out, cudaStream_t st) {
+    if (av.kind == CHEBFD_COMPLEX128)
+        run_colreduce<true, double2, 1>(ctx, av, v, lam, dev_out, st, static_cast<int>(av.width));
+    else if (av.width % 2 == 0)
+        run_colreduce<false, double2, 1>(ctx, av, v, lam, dev_out, st, static_cast<int>(av.width / 2));
+    else
+        run_colreduce<false, double, 1>(ctx, av, v, lam, dev_out, st, static_cast<int>(av.width));
+}
+
+void launch_axpy_scalar(Context& ctx, Block& w, const Block& q, double hr, double hi,
+                        cudaStream_t st) {
+    const int64_t n = w.rows * w.width;
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, ctx.num_sms * 8));
+    axpy_scalar_kernel<<<grid, 256, 0, st>>>(static_cast<double*>(w.owned()),
+                                             static_cast<const double*>(q.owned()), n, w.kind, hr,
+                                             hi);
+    CFD_CUDA(cudaGetLastError());
+    ctx.launches++;
+}
+
+void launch_scale_columns(Context& ctx, Block& b, const double* d_dev, cudaStream_t st) {
+    const int64_t n = b.rows * b.width * (b.kind ? 2 : 1);
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, ctx.num_sms * 8));
+    divcols_kernel<<<grid, 256, 0, st>>>(static_cast<double*>(b.owned()), b.rows, b.width, b.kind,
+                                         d_dev);
+    CFD_CUDA(cudaGetLastError());
+    ctx.launches++;
+}
+
+void launch_copy_columns(Context& ctx, Block& dst, int64_t d0, const Block& src, int64_t s0,
+                         int64_t n, cudaStream_t st) {
+    const int f = dst.kind ? 2 : 1;
+    const int64_t tot = dst.rows * n * f;
+    if (tot == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>((tot + 255) / 256, ctx.num_sms * 8));
+    copycols_kernel<<<grid, 256, 0, st>>>(static_cast<double*>(dst.owned()), dst.width * f, d0 * f,
+                                          static_cast<const double*>(src.owned()), src.width * f,
+                                          s0 * f, dst.rows, n * f);
+    CFD_CUDA(cudaGetLastError());
+    ctx.launches++;
+}
+
+void launch_philox_normal(Context& ctx, Block& b, uint64_t seed, cudaStream_t st) {
+    const int64_t n = b.rows * b.width * (b.kind ? 2 : 1);
+    if (n == 0) return;
+    const int grid = ctx.num_sms * 4;
+    // offset the Philox subsequence by the global first row so ranks differ
+    philox_normal_kernel<<<grid, 256, 0, st>>>(static_cast<double*>(b.owned()), n,
+                                               seed ^ (0x9E3779B97F4A7C15ULL * (b.row_begin + 1)));
+    CFD_CUDA(cudaGetLastError());
+    ctx.launches++;
+}
+
+void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d_cols,
+                const void* d_vals, cudaStream_t st) {
+    const int64_t rows = m.part.local;
+    m.nchunks = (rows + kChunk - 1) / kChunk;
+    m.chunk_ptr.ensure(sizeof(int64_t) * (m.nchunks + 1));
+    DeviceBuffer slots(sizeof(int64_t) * (m.nchunks + 1));
+    DeviceBuffer dmax(sizeof(int) * 2);
+    CFD_CUDA(cudaMemsetAsync(dmax.p, 0, sizeof(int) * 2, st));
+    CFD_CUDA(cudaMemsetAsync(slots.p, 0, sizeof(int64_t) * (m.nchunks + 1), st));
+    if (m.nchunks > 0) {
+        sell_width_kernel<<<static_cast<unsigned>((m.nchunks + 255) / 256), 256, 0, st>>>(
+            d_offs, rows, m.nchunks, slots.as<int64_t>(), dmax.as<int>());
+        CFD_CUDA(cudaGetLastError());
+    }
+    size_t tmp_bytes = 0;
+    CFD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, slots.as<int64_t>(),
+                                           m.chunk_ptr.as<int64_t>(), m.nchunks + 1, st));
+    DeviceBuffer tmp(std::max<size_t>(tmp_bytes, 16));
+    CFD_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, slots.as<int64_t>(),
+                                           m.chunk_ptr.as<int64_t>(), m.nchunks + 1, st));
+    int64_t entries = 0;
+    int maxlen = 0;
+    CFD_CUDA(cudaMemcpyAsync(&entries, m.chunk_ptr.as<int64_t>() + m.nchunks, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st));
+    CFD_CUDA(cudaMemcpyAsync(&maxlen, dmax.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CFD_CUDA(cudaStreamSynchronize(st));
+    m.entries = entries;
+    m.max_row_len = maxlen;
+    if (static_cast<int64_t>(m.part.ext_rows()) >= (1LL << 31))
+        fail(CHEBFD_ERR_UNSUPPORTED, "extended row count exceeds int32 column indices");
+    m.cols.ensure(sizeof(int) * std::max<int64_t>(entries, 1));
+    m.vals.ensure((m.kind ? 16 : 8) * std::max<int64_t>(entries, 1));
+    ColMap cm{m.part.row_begin, m.part.local, m.part.halo_lo, m.part.halo_hi, m.part.lo_src_begin,
+              m.part.hi_src_begin};
+    const int64_t threads = m.nchunks * kChunk;
+    if (threads > 0) {
+        const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+        if (m.kind)
+            sell_fill_kernel<double2><<<grid, 256, 0, st>>>(
+                d_offs, d_cols, static_cast<const double2*>(d_vals), rows,
+                m.chunk_ptr.as<int64_t>(), m.cols.as<int>(), m.vals.as<double2>(), cm,
+                dmax.as<int>() + 1);
+        else
+            sell_fill_kernel<double><<<grid, 256, 0, st>>>(
+                d_offs, d_cols, static_cast<const double*>(d_vals), rows,
+                m.chunk_ptr.as<int64_t>(), m.cols.as<int>(), m.vals.as<double>(), cm,
+                dmax.as<int>() + 1);
+        CFD_CUDA(cudaGetLastError());
+    }
+    int err = 0;
+    CFD_CUDA(cudaMemcpyAsync(&err, dmax.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CFD_CUDA(cudaStreamSynchronize(st));
+    if (err) fail(CHEBFD_ERR_UNSUPPORTED, "matrix column outside this rank's rows and halos");
+}
+
+}  // namespace cfd

@@ -1,0 +1,221 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle.
+
+Row-local results (spmmvm, fused step W/X, apply_filter X) are compared
+BIT-FOR-BIT: the kernels evaluate each entry with the reference's exact
+operation order (no FMA contraction), see kernels.cu header.  Reductions
+(dots, moments, Gram) differ only in summation order and are compared with a
+relative tolerance written in each test.
+"""
+import numpy as np
+import pytest
+
+import paper_1510_04895_b200 as cf
+
+pytestmark = pytest.mark.gpu
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def graphene(ctx, orc, lx, ly, disorder=0.1, seed=1, boundary="periodic_xy_open_z"):
+    A = cf.SparseMatrix.graphene(ctx, cf.LatticeSpec(lx, ly, disorder=disorder, seed=seed,
+                                                     boundary=boundary))
+    return A, orc.graphene(lx, ly, disorder=disorder, seed=seed, boundary=boundary)
+
+
+def ti(ctx, orc, l, disorder=0.5, seed=1, boundary="periodic_xy_open_z"):
+    A = cf.SparseMatrix.topological_insulator(
+        ctx, cf.LatticeSpec(*l, disorder=disorder, seed=seed, boundary=boundary))
+    return A, orc.topological_insulator(*l, disorder=disorder, seed=seed, boundary=boundary)
+
+
+def block(A, host):
+    return cf.BlockVector(A, host.shape[1]).upload(host)
+
+
+CASES = [
+    ("graphene", (8, 8), 5), ("graphene", (16, 16), 40), ("graphene", (13, 7), 1),
+    ("graphene", (16, 16), 3), ("ti", (4, 4, 4), 5), ("ti", (3, 5, 4), 32), ("ti", (4, 4, 4), 1),
+]
+
+
+def make_case(ctx, orc, name, l):
+    return graphene(ctx, orc, *l) if name == "graphene" else ti(ctx, orc, l)
+
+
+@pytest.mark.parametrize("name,l,nb", CASES)
+def test_spmmvm_bitexact(ctx, orc, name, l, nb):
+    A, c = make_case(ctx, orc, name, l)
+    x = orc.randomize(c.dim, nb, 11, name == "ti")
+    for alpha, beta in ((1.0, 0.0), (0.37, -0.21)):
+        y = cf.spmmvm(A, block(A, x), alpha, beta).to_numpy()
+        assert bits_equal(y, orc.spmmvm(c, x, alpha, beta))
+
+
+@pytest.mark.parametrize("name,l,nb", CASES)
+def test_fused_bitexact_and_dots(ctx, orc, name, l, nb):
+    A, c = make_case(ctx, orc, name, l)
+    cx = name == "ti"
+    u, w, x = (orc.randomize(c.dim, nb, s, cx) for s in (1, 2, 3))
+    U, W, X = block(A, u), block(A, w), block(A, x)
+    d = cf.spmmvm_fused(A, U, W, X, 0.37, -0.21, 0.83, dots=True)
+    dref = orc.spmmvm_fused(c, u, w, x, 0.37, -0.21, 0.83, want_dots=True)
+    assert bits_equal(W.to_numpy(), w)
+    assert bits_equal(X.to_numpy(), x)
+    # Kahan dots vs Kahan dots, different summation order: 1e-12 relative
+    # (test_core_linalg.cpp:152 uses 1e-12 against the unfused dots)
+    assert np.allclose(d, dref, rtol=1e-12, atol=1e-12 * np.max(np.abs(dref)))
+
+
+@pytest.mark.parametrize("name,l,nb", CASES[:5])
+def test_recurrence_step_bitexact(ctx, orc, name, l, nb):
+    A, c = make_case(ctx, orc, name, l)
+    cx = name == "ti"
+    u, w = (orc.randomize(c.dim, nb, s, cx) for s in (4, 5))
+    U, W = block(A, u), block(A, w)
+    cf.recurrence_step(A, U, W, 0.6, 0.1)
+    orc.recurrence_step(c, u, w, 0.6, 0.1)
+    assert bits_equal(W.to_numpy(), w)
+
+
+def test_axpy_bitexact(ctx, orc):
+    A, c = ti(ctx, orc, (3, 3, 3))
+    x, u, w = (orc.randomize(c.dim, 4, s, True) for s in (1, 2, 3))
+    X, U, W = block(A, x), block(A, u), block(A, w)
+    cf.block_axpy_scal(X, U, W, 0.2, -1.3, 0.7)
+    orc.block_axpy_scal(x, u, w, 0.2, -1.3, 0.7)
+    assert bits_equal(X.to_numpy(), x)
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+@pytest.mark.parametrize("name,l,nb,deg", [
+    ("graphene", (16, 16), 40, 50), ("graphene", (8, 8), 3, 7), ("ti", (4, 4, 4), 32, 40),
+    ("ti", (3, 3, 2), 5, 2), ("graphene", (8, 8), 1, 3)])
+def test_apply_filter_bitexact_with_moments(ctx, orc, name, l, nb, deg, graphs):
+    ctx.set_option("graphs", graphs)
+    try:
+        A, c = make_case(ctx, orc, name, l)
+        bounds = (-3.2, 3.3) if name == "graphene" else (-5.6, 5.6)
+        p = cf.make_filter((-0.2, 0.3), bounds, deg, "lanczos2")
+        x0 = orc.randomize(c.dim, nb, 9, name == "ti")
+        X = block(A, x0)
+        mom = cf.apply_filter(A, X, p, want_moments=True)
+        xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+        assert bits_equal(X.to_numpy(), xr)
+        # moments: plain sums in a different order; 1e-12 of the column norm
+        scale = np.max(np.abs(mr[0]))
+        assert np.max(np.abs(mom.m - mr)) <= 1e-12 * scale
+        # second call (graph replay / cache hit) with new coefficients
+        p2 = cf.make_filter((-0.1, 0.4), bounds, deg, "jackson")
+        X.upload(x0)
+        cf.apply_filter(A, X, p2)
+        xr2, _ = orc.apply_filter(c, x0, p2.combined, p2.alpha, p2.beta)
+        assert bits_equal(X.to_numpy(), xr2)
+    finally:
+        ctx.set_option("graphs", True)
+
+
+def test_apply_filter_host_e2e(ctx, orc):
+    A, c = ti(ctx, orc, (4, 4, 3))
+    p = cf.make_filter((-0.3, 0.3), (-5.6, 5.6), 30, "lanczos2")
+    x = orc.randomize(c.dim, 8, 3, True)
+    y = x.copy()
+    cf.apply_filter_host(A, y, p)
+    xr, _ = orc.apply_filter(c, x, p.combined, p.alpha, p.beta)
+    assert bits_equal(y, xr)
+
+
+def test_block_equals_independent_columns(ctx, orc):
+    """test_core_linalg.cpp:87-99 for the whole filter: columns never mix."""
+    A, c = ti(ctx, orc, (6, 6, 6))
+    p = cf.make_filter((-0.2, 0.2), (-5.6, 5.6), 60, "lanczos2")
+    x = orc.randomize(c.dim, 6, 21, True)
+    X = block(A, x)
+    cf.apply_filter(A, X, p)
+    full = X.to_numpy()
+    for k in (0, 3, 5):
+        Xk = block(A, np.ascontiguousarray(x[:, k:k + 1]))
+        cf.apply_filter(A, Xk, p)
+        assert bits_equal(Xk.to_numpy()[:, 0], full[:, k])
+
+
+def test_diagonal_filter_known_answer(ctx):
+    """test_filter.cpp:142-154: apply_filter on a diagonal = eval_scalar."""
+    lam = np.array([-0.8, -0.3, 0.0, 0.25, 0.6, 0.95])
+    A = cf.SparseMatrix.from_csr(ctx, 6, np.arange(7), np.arange(6), lam)
+    p = cf.make_filter((-0.1, 0.3), (-1.0, 1.0), 40, "lanczos2")
+    X = cf.BlockVector(A, 6).upload(2.0 * np.eye(6))
+    cf.apply_filter(A, X, p)
+    want = np.diag([2.0 * cf.eval_scalar(p, v) for v in lam])
+    assert np.max(np.abs(X.to_numpy() - want)) <= 1e-12
+
+
+def test_fused_coeff0_is_T2(ctx):
+    """test_core_linalg.cpp:101-116"""
+    d = np.array([-0.9, -0.3, 0.2, 0.8])
+    A = cf.SparseMatrix.from_csr(ctx, 4, np.arange(5), np.arange(4), d)
+    U = cf.BlockVector(A, 1).upload(d[:, None])
+    W = cf.BlockVector(A, 1).upload(np.ones((4, 1)))
+    X = cf.BlockVector(A, 1).upload(np.full((4, 1), 0.5))
+    cf.spmmvm_fused(A, U, W, X, 1.0, 0.0, 0.0)
+    assert np.allclose(W.to_numpy()[:, 0], 2 * d * d - 1, rtol=1e-15)
+    assert np.array_equal(X.to_numpy(), np.full((4, 1), 0.5))
+
+
+def test_fused_rejects_aliasing(ctx, orc):
+    """test_core_linalg.cpp:157-164"""
+    A, c = graphene(ctx, orc, 4, 4)
+    U = cf.BlockVector(A, 2).randomize(1)
+    W = cf.BlockVector(A, 2).randomize(2)
+    with pytest.raises(cf.InvalidArgument):
+        cf.spmmvm_fused(A, U, W, W, 1.0, 0.0, 0.5)
+    with pytest.raises(cf.InvalidArgument):
+        cf.spmmvm_fused(A, U, U, W, 1.0, 0.0, 0.5)
+
+
+def test_apply_filter_rejects_degree_below_2(ctx):
+    """test_filter.cpp:226-235"""
+    A = cf.SparseMatrix.from_csr(ctx, 2, np.arange(3), np.arange(2), np.array([0.0, 0.5]))
+    p = cf.make_filter((-0.5, 0.5), (-1.0, 1.0), 4, "none")
+    p.degree = 1
+    p.combined = p.combined[:2]
+    X = cf.BlockVector(A, 1).randomize(1)
+    with pytest.raises(cf.InvalidArgument):
+        cf.apply_filter(A, X, p)
+
+
+def test_randomize_matches_reference_stream(ctx, orc):
+    A, c = ti(ctx, orc, (3, 3, 3))
+    X = cf.BlockVector(A, 7).randomize(42)
+    assert bits_equal(X.to_numpy(), orc.randomize(c.dim, 7, 42, True))
+    B, cg = graphene(ctx, orc, 5, 5)
+    Y = cf.BlockVector(B, 3).randomize(5)
+    assert bits_equal(Y.to_numpy(), orc.randomize(cg.dim, 3, 5, False))
+
+
+@pytest.mark.parametrize("cx", [False, True])
+def test_reductions(ctx, orc, cx):
+    A, c = (ti(ctx, orc, (4, 4, 4)) if cx else graphene(ctx, orc, 16, 16))
+    x = orc.randomize(c.dim, 6, 1, cx)
+    y = orc.randomize(c.dim, 6, 2, cx)
+    X, Y = block(A, x), block(A, y)
+    assert rel(cf.column_dots(X, Y), orc.column_dots(x, y)) <= 1e-13
+    assert rel(cf.column_norms(X), orc.column_norms(x)) <= 1e-14
+    assert rel(cf.gram(X, Y), orc.gram(x, y)) <= 1e-13
+    b = orc.randomize(6, 4, 3, cx)
+    assert rel(cf.block_mult_small(X, b).to_numpy(), orc.block_mult_small(x, b)) <= 1e-13
+
+
+def test_gram_kahan_exact_count(ctx):
+    """test_core_linalg.cpp:399-403: gram of ones counts the dimension."""
+    n = 1000
+    A = cf.SparseMatrix.from_csr(ctx, n, np.arange(n + 1), np.arange(n), np.ones(n))
+    X = cf.BlockVector(A, 1).upload(np.ones((n, 1)))
+    assert cf.gram(X, X)[0, 0] == 1000.0
