@@ -134,6 +134,7 @@ def run_ours(args):
         ctx = cf.Context.distributed(local, rank, world, obj[0])
     else:
         ctx = cf.Context(local)
+    ctx.set_option("kernel", args.kernel)
     w = workload(args, world)
     spec = cf.LatticeSpec(w["lx"], w["ly"], w["lz"], disorder=w["disorder"], seed=w["seed"],
                           boundary=w["boundary"])
@@ -217,6 +218,7 @@ def run_ours(args):
                 else "single GPU",
                 "l2": "no flush: every block (537 MB) exceeds the 126 MB L2",
                 "hbm_gbs_model": round(achieved, 1),
+                "step_kernel": args.kernel,
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
@@ -320,6 +322,8 @@ def main():
     ap.add_argument("--nb", type=int, default=32)
     ap.add_argument("--degree", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel", default="tma", choices=["tma", "gather"],
+                    help="step kernel: TMA-staged SELL chunks (default) or plain register gathers")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     out = run_reference(args) if args.impl == "reference" else run_ours(args)

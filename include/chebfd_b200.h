@@ -1,7 +1,7 @@
 /* chebfd_b200 -- B200-native ChebFD hot path behind a plain C ABI.
  *
  * This is the drop-in boundary.  The reference has no FFI; its
- * boundary is the C++ template API in /root/reference/proj/include/chebfd/*.hpp
+ * boundary is the C++ template API in /root/reference/proj/include/chebfd/ headers
  * instantiated for double and std::complex<double>.  Each entry point below
  * names the reference function it replaces (file:line relative to
  * /root/reference/proj).  include/chebfd_b200.hpp restores the reference's
@@ -76,8 +76,9 @@ int chebfd_ctx_info(chebfd_ctx* ctx, int* device, int* rank, int* nranks, int* n
 int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count);
 /* Options: CHEBFD_OPT_GRAPHS (1 = capture apply_filter into cached CUDA
  * graphs, default 1); CHEBFD_OPT_OVERLAP (1 = overlap the halo exchange with
- * interior rows, default 1). */
-enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2 };
+ * interior rows, default 1); CHEBFD_OPT_KERNEL (step kernel variant: 0 plain
+ * register gathers, 1 TMA-staged SELL chunks with pre-scaled values; default 1). */
+enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3 };
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */

@@ -11,6 +11,7 @@ DomainError (ValueError), std::out_of_range -> OutOfRange (IndexError).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -82,10 +83,14 @@ class Context:
 
     def __init__(self, device: int = 0, _handle=None):
         self._h = C.c_void_p()
+        self._children = weakref.WeakSet()  # matrices / blocks to release first
         if _handle is None:
             _check(_lib().chebfd_ctx_create(device, C.byref(self._h)))
         else:
             self._h = _handle
+
+    def _adopt(self, obj):
+        self._children.add(obj)
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -101,7 +106,14 @@ class Context:
         return cls(_handle=h)
 
     def close(self):
+        """Release every block and matrix of this context, then the context."""
         if getattr(self, "_h", None) and self._h.value:
+            kids = list(self._children)
+            for k in kids:  # blocks before matrices (blocks reference matrices)
+                if isinstance(k, BlockVector):
+                    k.close()
+            for k in kids:
+                k.close()
             _lib().chebfd_ctx_destroy(self._h)
             self._h = C.c_void_p()
 
@@ -141,7 +153,10 @@ class Context:
         return ms.value
 
     def set_option(self, name: str, value):
-        code = {"graphs": 1, "overlap": 2}[name]
+        """graphs (bool), overlap (bool), kernel ("gather" | "tma")."""
+        code = {"graphs": 1, "overlap": 2, "kernel": 3}[name]
+        if name == "kernel" and isinstance(value, str):
+            value = {"gather": 0, "tma": 1}[value]
         _check(_lib().chebfd_ctx_set_option(self._h, code, int(value)))
 
 
@@ -248,6 +263,7 @@ class SparseMatrix:
     def __init__(self, ctx: Context, handle):
         self.ctx = ctx
         self._h = handle
+        ctx._adopt(self)
         info = L.chebfd_matrix_info()
         _check(_lib().chebfd_matrix_get_info(self._h, C.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in L.chebfd_matrix_info._fields_}
@@ -339,6 +355,7 @@ class BlockVector:
             self._h = C.c_void_p()
             _check(_lib().chebfd_block_create_dim(ctx._h, kind, dim, width, C.byref(self._h)))
         self.ctx = ctx if ctx is not None else A.ctx
+        self.ctx._adopt(self)
         k, r, w, rb = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
         _check(_lib().chebfd_block_info(self._h, C.byref(k), C.byref(r), C.byref(w), C.byref(rb)))
         self.kind, self.rows, self.width_, self.row_begin = k.value, r.value, w.value, rb.value

@@ -448,6 +448,15 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
     const bool moments = moments_host != nullptr;
     const int64_t nb = x.width;
     FilterWorkspace& ws = filter_workspace(c, a, nb, moments);
+    Matrix& am = const_cast<Matrix&>(a);
+    if (c.kernel_variant == 1) {  // pre-scaled values for the start step (alpha) and 2 alpha steps
+        ensure_scaled_values(c, am, alpha, c.stream);
+        ensure_scaled_values(c, am, 2.0 * alpha, c.stream);
+        if (am.scaled_evicted) {
+            purge_graphs(c, &a, nullptr);
+            am.scaled_evicted = false;
+        }
+    }
     GraphKey key{&a, x.owned(), degree, 0, 0, moments, nb};
     std::memcpy(&key.alpha_bits, &alpha, 8);
     std::memcpy(&key.beta_bits, &beta, 8);
@@ -561,8 +570,9 @@ static void ctx_init(Context& c, int device) {
     c.cublas = reinterpret_cast<cublasContext*>(h);
     cublas_check(cublasSetStream(h, c.stream), "cublasSetStream");
     // reduction scratch sized for the largest persistent grid (no allocation
-    // inside graph capture): grid <= 8 CTAs/SM, 2 dots x 256 units x 16 B
-    c.partials.ensure(static_cast<size_t>(c.num_sms) * 8 * 2 * 256 * 16);
+    // inside graph capture): grid <= 8 CTAs/SM, up to 3 launches per step,
+    // 2 dots x 256 units x 16 B
+    c.partials.ensure(static_cast<size_t>(c.num_sms) * 8 * 3 * 2 * 256 * 16);
     c.counter.ensure(256);
     CFD_CUDA(cudaMemsetAsync(c.counter.p, 0, 256, c.stream));
     c.dscratch.ensure(1 << 20);
@@ -631,6 +641,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->use_graphs = value != 0;
         else if (option == CHEBFD_OPT_OVERLAP)
             c->overlap = value != 0;
+        else if (option == CHEBFD_OPT_KERNEL)
+            c->kernel_variant = static_cast<int>(value);
         else
             fail(CHEBFD_ERR_INVALID_ARGUMENT, "unknown option");
     });

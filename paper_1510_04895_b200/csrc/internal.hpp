@@ -80,6 +80,10 @@ struct Matrix {
     DeviceBuffer chunk_ptr;  // int64[nchunks+1], slot offsets
     DeviceBuffer cols;       // int32[entries], extended-row index or -1 padding
     DeviceBuffer vals;       // double or double2 [entries]
+    // value copies pre-multiplied by a step's alpha (apply_filter uses alpha
+    // and 2 alpha); at most 4 are kept
+    std::vector<std::pair<double, std::unique_ptr<DeviceBuffer>>> scaled;
+    bool scaled_evicted = false;
 };
 
 // ---- block vector -------------------------------------------------------------------
@@ -137,6 +141,7 @@ struct Context {
     cusolverDnContext* cusolver = nullptr;
     ncclComm_t nccl = nullptr;
     bool use_graphs = true, overlap = true;
+    int kernel_variant = 1;  // step kernel: 0 register gathers, 1 TMA-staged matrix chunks
     int64_t launches = 0;
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
     DeviceBuffer partials;   // per-block partial sums
@@ -182,6 +187,8 @@ struct StepArgs {
 };
 void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st);
 
+// cache a copy of a's values multiplied by s (used by the v3 step kernel)
+void ensure_scaled_values(Context& ctx, Matrix& a, double s, cudaStream_t st);
 void launch_axpy(Context& ctx, Block& x, const Block& u, const Block& w, double c0, double c1,
                  double c2, cudaStream_t st);
 // out[k] = sum_i f(x_ik, y_ik) over owned rows; mode 0: conj(x) y (S), 1: |x|^2 (double)

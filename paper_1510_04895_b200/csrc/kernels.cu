@@ -203,6 +203,7 @@ struct StepParams {
     const int64_t* chunk_ptr;
     const int* cols;
     const void* vals;
+    const void* svals;    // values pre-multiplied by `alpha` (or null)
     int64_t row0, row1;   // owned rows of this launch
     int64_t halo_lo;      // extended-row offset of owned row 0
     int pitch;            // units per row in memory
@@ -226,12 +227,95 @@ struct StepParams {
     unsigned* counter;
 };
 
-template <bool CPLX, class T, int KIND, int DMODE>
-__global__ void __launch_bounds__(256) step_kernel(const StepParams p) {
+// Sum_j (a_rj * scale) * in[c_rj] over one row, in the row's stored order.
+// MAXW > 0: all column indices of the row are loaded first, then every
+// gather is issued before the first use (maximum memory-level parallelism).
+template <class O, class T, class M, int MAXW>
+__device__ __forceinline__ T gather_row(const int* __restrict__ cols, const M* __restrict__ vals,
+                                        const T* __restrict__ in, int64_t base, int width, int lane,
+                                        int pitch, int64_t col_off, double scale) {
+    T acc = O::zero();
+    if constexpr (MAXW > 0) {
+        int c[MAXW];
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j)
+            c[j] = (j < width) ? __ldg(&cols[base + static_cast<int64_t>(j) * 32 + lane]) : -1;
+        T g[MAXW];
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j)
+            if (c[j] >= 0) g[j] = ldg(&in[static_cast<int64_t>(c[j]) * pitch + col_off]);
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j)
+            if (c[j] >= 0) {
+                const M v = __ldg(&vals[base + static_cast<int64_t>(j) * 32 + lane]);
+                acc = O::vadd(acc, O::prod(O::scale(v, scale), g[j]));
+            }
+    } else {
+        constexpr int BATCH = 8;
+        for (int j0 = 0; j0 < width; j0 += BATCH) {
+            int c[BATCH];
+            T g[BATCH];
+#pragma unroll
+            for (int b = 0; b < BATCH; ++b)
+                c[b] = (j0 + b < width) ? __ldg(&cols[base + static_cast<int64_t>(j0 + b) * 32 + lane]) : -1;
+#pragma unroll
+            for (int b = 0; b < BATCH; ++b)
+                if (c[b] >= 0) g[b] = ldg(&in[static_cast<int64_t>(c[b]) * pitch + col_off]);
+#pragma unroll
+            for (int b = 0; b < BATCH; ++b)
+                if (c[b] >= 0) {
+                    const M v = __ldg(&vals[base + static_cast<int64_t>(j0 + b) * 32 + lane]);
+                    acc = O::vadd(acc, O::prod(O::scale(v, scale), g[b]));
+                }
+        }
+    }
+    return acc;
+}
+
+// Per-entry epilogue of each step kind, in the reference's operation order.
+template <class O, class T, int KIND, int DMODE, int NA>
+__device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T wi, const T xi,
+                                              const T x0v, int64_t own, T* __restrict__ W,
+                                              T* __restrict__ X, T* __restrict__ X0, double beta,
+                                              double coeff, double c1, double c2, T (&acc_d)[NA],
+                                              T (&comp_d)[NA]) {
+    if constexpr (KIND == kStepSpmmvm) {
+        T y = acc;
+        if (beta != 0.0) y = O::vadd(y, O::smul(beta, ui));  // kernels.hpp:62-65
+        st_stream(&W[own], y);
+        if constexpr (DMODE == 3) {  // apply_filter entry: x0 = X, m0 = <x,x>, m1 = <x,u>
+            st_stream(&X0[own], ui);
+            acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, ui));
+            acc_d[1] = O::vadd(acc_d[1], O::cdot(ui, y));
+        }
+    } else if constexpr (KIND == kStepStart2) {
+        // w = spmmvm(A,u,2a,2b); w = 1*w + (-1)*x + 0*x; x = c0 x + c1 u + c2 w  (filter.hpp:93-103)
+        T wr = acc;
+        if (beta != 0.0) wr = O::vadd(wr, O::smul(beta, ui));
+        const T wn = O::vadd(O::vadd(O::smul(1.0, wr), O::smul(-1.0, xi)), O::smul(0.0, xi));
+        st_stream(&W[own], wn);
+        if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(xi, wn));
+        const T xn = O::vadd(O::vadd(O::smul(coeff, xi), O::smul(c1, ui)), O::smul(c2, wn));
+        st_stream(&X[own], xn);
+    } else {
+        // fused / recur: w' = tmp + 2b u_i - w_i  (kernels.hpp:103,142)
+        const T wn = O::vsub(O::vadd(acc, O::smul(beta, ui)), wi);
+        st_stream(&W[own], wn);
+        if constexpr (KIND == kStepFused) {
+            if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
+            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+            st_stream(&X[own], O::vadd(xi, O::smul(coeff, wn)));  // kernels.hpp:106
+        } else {
+            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+        }
+    }
+}
+
+template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
+__global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
     constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
-    constexpr int BATCH = 4;
     const int t = threadIdx.x;
     const int rr = t / p.US;
     const int u = t - rr * p.US;
@@ -264,72 +348,21 @@ __global__ void __launch_bounds__(256) step_kernel(const StepParams p) {
         const int64_t rl = rg * R + rr;
         if (rl >= nrows) continue;
         const int64_t r = p.row0 + rl;  // owned row
+        const int64_t own = r * p.pitch + col_off;
+        // own-row streams first: independent of the gathers, so they overlap
+        T wi{}, xi{}, x0v{};
+        if constexpr (KIND == kStepFused || KIND == kStepRecur) wi = ld_stream(&W[own]);
+        if constexpr (KIND == kStepFused || KIND == kStepStart2) xi = ld_stream(&X[own]);
+        if constexpr (DMODE == 2 && KIND != kStepStart2) x0v = ld_stream(&X0[own]);
         const int64_t chunk = r >> 5;
         const int lane = static_cast<int>(r & 31);
         const int64_t base = __ldg(&p.chunk_ptr[chunk]);
         const int width = static_cast<int>((__ldg(&p.chunk_ptr[chunk + 1]) - base) >> 5);
-        T acc = O::zero();
-        for (int j0 = 0; j0 < width; j0 += BATCH) {
-            int c[BATCH];
-            M v[BATCH];
-            T g[BATCH];
-#pragma unroll
-            for (int b = 0; b < BATCH; ++b) {
-                c[b] = -1;
-                if (j0 + b < width) {
-                    const int64_t idx = base + static_cast<int64_t>(j0 + b) * 32 + lane;
-                    c[b] = __ldg(&cols[idx]);
-                    v[b] = __ldg(&vals[idx]);
-                }
-            }
-#pragma unroll
-            for (int b = 0; b < BATCH; ++b)
-                if (c[b] >= 0) g[b] = ldg(&in[static_cast<int64_t>(c[b]) * p.pitch + col_off]);
-#pragma unroll
-            for (int b = 0; b < BATCH; ++b)
-                if (c[b] >= 0) acc = O::vadd(acc, O::prod(O::scale(v[b], p.alpha), g[b]));
-        }
-        const int64_t own = r * p.pitch + col_off;
+        const T acc = gather_row<O, T, M, MAXW>(cols, vals, in, base, width, lane, p.pitch, col_off,
+                                                p.alpha);
         const T ui = ldg(&in[(r + p.halo_lo) * p.pitch + col_off]);
-        if constexpr (KIND == kStepSpmmvm) {
-            T y = acc;
-            if (p.beta != 0.0) y = O::vadd(y, O::smul(p.beta, ui));
-            st_stream(&W[own], y);
-            if constexpr (DMODE == 3) {  // apply_filter entry: x0 = X, m0 = <x,x>, m1 = <x,u>
-                st_stream(&X0[own], ui);
-                acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, ui));
-                acc_d[1] = O::vadd(acc_d[1], O::cdot(ui, y));
-            }
-        } else if constexpr (KIND == kStepStart2) {
-            // w = spmmvm(A,u,2a,2b); w = 1*w + (-1)*x + 0*x; x = c0 x + c1 u + c2 w
-            T wr = acc;
-            if (p.beta != 0.0) wr = O::vadd(wr, O::smul(p.beta, ui));
-            const T xi = ld_stream(&X[own]);
-            const T wn = O::vadd(O::vadd(O::smul(1.0, wr), O::smul(-1.0, xi)), O::smul(0.0, xi));
-            st_stream(&W[own], wn);
-            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(xi, wn));
-            const T xn = O::vadd(O::vadd(O::smul(coeff, xi), O::smul(c1, ui)), O::smul(c2, wn));
-            st_stream(&X[own], xn);
-        } else {
-            // fused / recur: w' = tmp + 2b u_i - w_i
-            const T wi = ld_stream(&W[own]);
-            const T wn = O::vsub(O::vadd(acc, O::smul(p.beta, ui)), wi);
-            st_stream(&W[own], wn);
-            if constexpr (KIND == kStepFused) {
-                const T xi = ld_stream(&X[own]);
-                if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
-                if constexpr (DMODE == 2) {
-                    const T x0 = ld_stream(&X0[own]);
-                    acc_d[0] = O::vadd(acc_d[0], O::cdot(x0, wn));
-                }
-                st_stream(&X[own], O::vadd(xi, O::smul(coeff, wn)));
-            } else {
-                if constexpr (DMODE == 2) {
-                    const T x0 = ld_stream(&X0[own]);
-                    acc_d[0] = O::vadd(acc_d[0], O::cdot(x0, wn));
-                }
-            }
-        }
+        step_epilogue<O, T, KIND, DMODE>(acc, ui, wi, xi, x0v, own, W, X, X0, p.beta, coeff, c1, c2,
+                                         acc_d, comp_d);
     }
 
     if constexpr (NDOT > 0) {
@@ -350,6 +383,183 @@ __global__ void __launch_bounds__(256) step_kernel(const StepParams p) {
                                                  uoff + uu, v);
                              });
     }
+}
+
+// ---- TMA-staged step kernel (default) ----------------------------------------------------
+// A CTA walks over tiles of TR = max(32, R) rows (whole SELL chunks).  The
+// tile's column indices and values -- contiguous in SELL -- are brought into
+// shared memory by two TMA bulk copies (cp.async.bulk + mbarrier tx count),
+// double-buffered so tile k+1 streams in while tile k is processed.  Threads
+// read indices/values from shared memory, so registers only hold the
+// gathered neighbour units in flight.  Own-row streams (W, X, x0) are plain
+// coalesced loads issued ahead of the gathers.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LAB_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LAB_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+template <bool CPLX, class T, int KIND, int DMODE, int MAXW, bool PRESCALED>
+__global__ void __launch_bounds__(256, 2) step_tma_kernel(const StepParams p) {
+    using O = Ops<CPLX, T>;
+    using M = typename O::M;
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2];
+    const int t = threadIdx.x;
+    const int US = p.US;
+    const int rr = t / US;
+    const int u = t - rr * US;
+    const int R = p.R;
+    const int TR = R > 32 ? R : 32;  // rows per tile (whole chunks)
+    const int NCH = TR / 32;
+    const int cap = MAXW * TR;  // slots per buffer
+    int* cols_s = reinterpret_cast<int*>(smem_raw);
+    M* vals_s = reinterpret_cast<M*>(smem_raw + ((2 * cap * sizeof(int) + 15) & ~size_t(15)));
+
+    const int cu = p.u_off + u;
+    const T* __restrict__ inu = static_cast<const T*>(p.in) + cu;
+    T* __restrict__ W = static_cast<T*>(p.w) + cu;
+    T* __restrict__ X = static_cast<T*>(p.x) + cu;
+    T* __restrict__ X0 = static_cast<T*>(p.x0) + cu;
+    const M* __restrict__ gvals = static_cast<const M*>(PRESCALED ? p.svals : p.vals);
+    const int pitch = p.pitch;
+    const int64_t halo = p.halo_lo;
+    const double alpha = p.alpha;
+    double coeff = p.c0, c1 = p.c1, c2 = p.c2;
+    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepStart2 && p.coeff_dev) {
+        coeff = p.coeff_dev[0];
+        c1 = p.coeff_dev[1];
+        c2 = p.coeff_dev[2];
+    }
+    T acc_d[NDOT > 0 ? NDOT : 1];
+    T comp_d[NDOT > 0 ? NDOT : 1];
+#pragma unroll
+    for (int d = 0; d < (NDOT > 0 ? NDOT : 1); ++d) {
+        acc_d[d] = O::zero();
+        comp_d[d] = O::zero();
+    }
+
+    const int64_t row0 = p.row0, row1 = p.row1;
+    const int64_t cbeg = row0 >> 5;
+    const int64_t cend = (row1 + 31) >> 5;
+    const int64_t ntiles = row1 > row0 ? (cend - cbeg + NCH - 1) / NCH : 0;
+    const int64_t* __restrict__ cptr = p.chunk_ptr;
+
+    auto issue = [&](int64_t tile, int buf) {
+        const int64_t c0 = cbeg + tile * NCH;
+        const int64_t c1e = min(c0 + NCH, cend);
+        const int64_t s0 = cptr[c0], s1 = cptr[c1e];
+        const unsigned n = static_cast<unsigned>(s1 - s0);
+        const unsigned bc = n * 4u, bv = n * static_cast<unsigned>(sizeof(M));
+        mbar_arrive_expect_tx(&bars[buf], bc + bv);
+        if (n) {
+            tma_load_1d(cols_s + buf * cap, p.cols + s0, bc, &bars[buf]);
+            tma_load_1d(vals_s + buf * cap, gvals + s0, bv, &bars[buf]);
+        }
+    };
+
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    int64_t tile = blockIdx.x;
+    if (t == 0 && tile < ntiles) issue(tile, 0);
+    unsigned phases = 0u;  // bit b = parity of buffer b's next completion
+    for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+        const int buf = k & 1;
+        if (t == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
+        mbar_wait(&bars[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        const int64_t c0 = cbeg + tile * NCH;
+        const int64_t sbase = cptr[c0];
+        const int* cs = cols_s + buf * cap;
+        const M* vs = vals_s + buf * cap;
+        for (int it = 0; it < TR; it += R) {
+            const int64_t r = c0 * 32 + it + rr;
+            if (r < row0 || r >= row1) continue;
+            const int64_t chunk = r >> 5;
+            const int lane = static_cast<int>(r & 31);
+            const int coff = static_cast<int>(__ldg(&cptr[chunk]) - sbase) + lane;
+            const int w = static_cast<int>((__ldg(&cptr[chunk + 1]) - __ldg(&cptr[chunk])) >> 5);
+            const int64_t own = r * pitch;
+            T wi{}, xi{}, x0v{};
+            if constexpr (KIND == kStepFused || KIND == kStepRecur) wi = ld_stream(&W[own]);
+            if constexpr (KIND == kStepFused || KIND == kStepStart2) xi = ld_stream(&X[own]);
+            if constexpr (DMODE == 2 && KIND != kStepStart2) x0v = ld_stream(&X0[own]);
+            int c[MAXW];
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j) c[j] = (j < w) ? cs[coff + j * 32] : -1;
+            T g[MAXW];
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j)
+                if (c[j] >= 0) g[j] = ldg(&inu[static_cast<int64_t>(c[j]) * pitch]);
+            const T ui = ldg(&inu[(r + halo) * pitch]);
+            T acc = O::zero();
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j)
+                if (c[j] >= 0) {
+                    const M v = vs[coff + j * 32];
+                    acc = O::vadd(acc, O::prod(PRESCALED ? v : O::scale(v, alpha), g[j]));
+                }
+            step_epilogue<O, T, KIND, DMODE>(acc, ui, wi, xi, x0v, own, W, X, X0, p.beta, coeff,
+                                             c1, c2, acc_d, comp_d);
+        }
+        __syncthreads();  // buffer `buf` is refilled two tiles later
+    }
+
+    if constexpr (NDOT > 0) {
+        T acc_out[NDOT];
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) acc_out[d] = acc_d[d];
+        const int uoff = p.u_off;
+        void* outp = p.dots_out;
+        const int64_t dstride = p.dots_row_stride;
+        grid_reduce<T, NDOT>(acc_out, R, US, static_cast<T*>(p.partials), p.part_base + blockIdx.x,
+                             p.nparts, p.final_launch != 0, p.counter,
+                             [&](int d, int uu, T vv) {
+                                 if (DMODE == 1)
+                                     O::store_full(static_cast<T*>(outp), uoff + uu, vv);
+                                 else
+                                     O::store_re(static_cast<double*>(outp) + d * dstride,
+                                                 uoff + uu, vv);
+                             });
+    }
+}
+
+// values pre-multiplied by s (one rounding per entry, as kernels.hpp:95)
+__global__ void scale_values_kernel(double* __restrict__ out, const double* __restrict__ in,
+                                    int64_t n, double s) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = mul(in[i], s);
 }
 
 // ---- generic per-column reductions ------------------------------------------------------
@@ -514,6 +724,23 @@ inline Geometry geometry(int units) {
     return g;
 }
 
+const void* find_scaled(const Matrix& a, double s) {
+    for (const auto& e : a.scaled)
+        if (e.first == s) return e.second->p;
+    return nullptr;
+}
+
+// rows per CTA iteration as a power of two (tiles of whole 32-row chunks)
+inline Geometry geometry_pow2(int units) {
+    Geometry g;
+    g.US = units;
+    int r = 1;
+    while (r * 2 * units <= 256) r *= 2;
+    g.R = r;
+    g.threads = r * units;
+    return g;
+}
+
 template <class K>
 int max_blocks_for(K kernel, int threads, size_t smem, int num_sms) {
     int per_sm = 0;
@@ -521,18 +748,37 @@ int max_blocks_for(K kernel, int threads, size_t smem, int num_sms) {
     return std::max(1, per_sm) * num_sms;
 }
 
-template <bool CPLX, class T, int KIND, int DMODE>
+template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
     const Matrix& a = *s.a;
     constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
     const int64_t nrows = s.row1 - s.row0;
-    auto kernel = step_kernel<CPLX, T, KIND, DMODE>;
+    constexpr int MW = MAXW > 0 ? MAXW : 4;
+    const bool tma = MAXW > 0 && ctx.kernel_variant == 1;
+    const void* svals = tma ? find_scaled(a, s.alpha) : nullptr;
+    auto kernel = tma ? (svals ? step_tma_kernel<CPLX, T, KIND, DMODE, MW, true>
+                               : step_tma_kernel<CPLX, T, KIND, DMODE, MW, false>)
+                      : step_kernel<CPLX, T, KIND, DMODE, MAXW>;
     int used_total = 0;
     // column slabs of at most 256 units (one CTA row-group spans a slab)
     for (int u0 = 0; u0 < units; u0 += 256) {
         const int us = std::min(256, units - u0);
-        Geometry g = geometry(us);
-        const size_t smem = NDOT * static_cast<size_t>(g.threads) * sizeof(T);
+        Geometry g = tma ? geometry_pow2(us) : geometry(us);
+        const int TR = std::max(32, g.R);
+        const size_t stage = tma ? 2 * static_cast<size_t>(MW) * TR : 0;
+        const size_t ring = tma ? ((stage * sizeof(int) + 15) & ~size_t(15)) +
+                                      stage * (CPLX ? 16 : 8)
+                                : 0;
+        const size_t smem = std::max(NDOT * static_cast<size_t>(g.threads) * sizeof(T), ring);
+        if (smem > 48 * 1024) {
+            static thread_local std::map<const void*, size_t> attr_set;
+            auto& cur = attr_set[reinterpret_cast<const void*>(kernel)];
+            if (cur < smem) {
+                CFD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem)));
+                cur = smem;
+            }
+        }
         static thread_local std::map<std::pair<const void*, int>, int> occ_cache;
         auto key = std::make_pair(reinterpret_cast<const void*>(kernel), g.threads);
         auto it = occ_cache.find(key);
@@ -543,12 +789,14 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         } else {
             maxb = it->second;
         }
-        const int64_t need = (nrows + g.R - 1) / g.R;
+        const int64_t need = tma ? (((s.row1 + 31) >> 5) - (s.row0 >> 5) + TR / 32 - 1) / (TR / 32)
+                                 : (nrows + g.R - 1) / g.R;
         const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, maxb)));
         StepParams p{};
         p.chunk_ptr = a.chunk_ptr.as<int64_t>();
         p.cols = a.cols.as<int>();
         p.vals = a.vals.p;
+        p.svals = svals;
         p.row0 = s.row0;
         p.row1 = s.row1;
         p.halo_lo = a.part.halo_lo;
@@ -593,24 +841,34 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     if (s.grid_used) *s.grid_used = used_total;
 }
 
-template <bool CPLX, class T>
-void dispatch_kind(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
+template <bool CPLX, class T, int MAXW>
+void dispatch_kind_w(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
     switch (s.kind_step) {
         case kStepSpmmvm:
-            if (s.dots_mode == 3) return run_step<CPLX, T, kStepSpmmvm, 3>(ctx, s, st, units, pitch);
-            return run_step<CPLX, T, kStepSpmmvm, 0>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 3) return run_step<CPLX, T, kStepSpmmvm, 3, MAXW>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepSpmmvm, 0, MAXW>(ctx, s, st, units, pitch);
         case kStepStart2:
-            if (s.dots_mode == 2) return run_step<CPLX, T, kStepStart2, 2>(ctx, s, st, units, pitch);
-            return run_step<CPLX, T, kStepStart2, 0>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepStart2, 2, MAXW>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepStart2, 0, MAXW>(ctx, s, st, units, pitch);
         case kStepFused:
-            if (s.dots_mode == 1) return run_step<CPLX, T, kStepFused, 1>(ctx, s, st, units, pitch);
-            if (s.dots_mode == 2) return run_step<CPLX, T, kStepFused, 2>(ctx, s, st, units, pitch);
-            return run_step<CPLX, T, kStepFused, 0>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 1) return run_step<CPLX, T, kStepFused, 1, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepFused, 2, MAXW>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepFused, 0, MAXW>(ctx, s, st, units, pitch);
         case kStepRecur:
-            if (s.dots_mode == 2) return run_step<CPLX, T, kStepRecur, 2>(ctx, s, st, units, pitch);
-            return run_step<CPLX, T, kStepRecur, 0>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepRecur, 2, MAXW>(ctx, s, st, units, pitch);
+            return run_step<CPLX, T, kStepRecur, 0, MAXW>(ctx, s, st, units, pitch);
     }
     fail(CHEBFD_ERR_INVALID_ARGUMENT, "bad step kind");
+}
+
+// Row-width buckets: graphene rows have 4 entries, TI rows 10-11.
+template <bool CPLX, class T>
+void dispatch_kind(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
+    const int w = s.a->max_row_len;
+    if (w <= 4) return dispatch_kind_w<CPLX, T, 4>(ctx, s, st, units, pitch);
+    if (w <= 12) return dispatch_kind_w<CPLX, T, 12>(ctx, s, st, units, pitch);
+    if (w <= 16) return dispatch_kind_w<CPLX, T, 16>(ctx, s, st, units, pitch);
+    return dispatch_kind_w<CPLX, T, 0>(ctx, s, st, units, pitch);
 }
 
 }  // namespace
@@ -627,6 +885,21 @@ void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st) {
     } else {
         dispatch_kind<false, double>(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
     }
+}
+
+void ensure_scaled_values(Context& ctx, Matrix& a, double s, cudaStream_t st) {
+    if (find_scaled(a, s)) return;
+    if (a.scaled.size() >= 4) {
+        // graphs may reference the evicted copy: the caller purges them
+        a.scaled.erase(a.scaled.begin());
+        a.scaled_evicted = true;
+    }
+    const int64_t n = std::max<int64_t>(a.entries, 1) * (a.kind ? 2 : 1);
+    auto buf = std::make_unique<DeviceBuffer>(sizeof(double) * n);
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, ctx.num_sms * 8));
+    scale_values_kernel<<<grid, 256, 0, st>>>(buf->as<double>(), a.vals.as<double>(), n, s);
+    CFD_CUDA(cudaGetLastError());
+    a.scaled.emplace_back(s, std::move(buf));
 }
 
 void launch_axpy(Context& ctx, Block& x, const Block& u, const Block& w, double c0, double c1,
