@@ -175,6 +175,20 @@ void allreduce_sum(Context& c, double* dev, size_t n, cudaStream_t st) {
 // One Chebyshev-type step over all owned rows, with the halo exchange of the
 // gathered operand overlapped with the interior rows when distributed.
 void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
+    if (c.kernel_variant == 1 && s.alpha != 1.0) {
+        // the TMA step kernel reads values pre-multiplied by alpha; build the
+        // copy now unless a graph is being captured (apply_filter pre-builds)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CFD_CUDA(cudaStreamIsCapturing(c.stream, &cs));
+        if (cs == cudaStreamCaptureStatusNone) {
+            Matrix& am = const_cast<Matrix&>(a);
+            ensure_scaled_values(c, am, s.alpha, c.stream);
+            if (am.scaled_evicted) {
+                purge_graphs(c, &a, nullptr);
+                am.scaled_evicted = false;
+            }
+        }
+    }
     s.a = &a;
     s.width_cols = gathered.width;
     s.in = gather_base(a, gathered);

@@ -78,6 +78,7 @@ struct Matrix {
     int64_t nchunks = 0;
     int64_t entries = 0;     // SELL slots (padding included)
     DeviceBuffer chunk_ptr;  // int64[nchunks+1], slot offsets
+    DeviceBuffer chunk_full; // uint8[nchunks]: every row has exactly the chunk width
     DeviceBuffer cols;       // int32[entries], extended-row index or -1 padding
     DeviceBuffer vals;       // double or double2 [entries]
     // value copies pre-multiplied by a step's alpha (apply_filter uses alpha

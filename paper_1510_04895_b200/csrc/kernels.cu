@@ -21,6 +21,7 @@
 #include <curand_kernel.h>
 
 #include <cub/device/device_scan.cuh>
+#include <type_traits>
 
 #include "internal.hpp"
 
@@ -201,6 +202,7 @@ __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1],
 // ---- the Chebyshev step kernel --------------------------------------------------------
 struct StepParams {
     const int64_t* chunk_ptr;
+    const unsigned char* chunk_full;  // 1: every row of the chunk has exactly `width` entries
     const int* cols;
     const void* vals;
     const void* svals;    // values pre-multiplied by `alpha` (or null)
@@ -423,7 +425,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
         : "memory");
 }
 
-template <bool CPLX, class T, int KIND, int DMODE, int MAXW, bool PRESCALED>
+template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 __global__ void __launch_bounds__(256, 2) step_tma_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
@@ -446,10 +448,9 @@ __global__ void __launch_bounds__(256, 2) step_tma_kernel(const StepParams p) {
     T* __restrict__ W = static_cast<T*>(p.w) + cu;
     T* __restrict__ X = static_cast<T*>(p.x) + cu;
     T* __restrict__ X0 = static_cast<T*>(p.x0) + cu;
-    const M* __restrict__ gvals = static_cast<const M*>(PRESCALED ? p.svals : p.vals);
+    const M* __restrict__ gvals = static_cast<const M*>(p.svals);  // pre-multiplied by alpha
     const int pitch = p.pitch;
     const int64_t halo = p.halo_lo;
-    const double alpha = p.alpha;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
     if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
     if (KIND == kStepStart2 && p.coeff_dev) {
@@ -484,6 +485,53 @@ __global__ void __launch_bounds__(256, 2) step_tma_kernel(const StepParams p) {
         }
     };
 
+    // one row of the current tile; FAST: every chunk of the tile is full with
+    // width MAXW (no padding predicates, slot offsets computed, not loaded)
+    auto row = [&](auto fast_tag, int64_t r, int64_t c0, int64_t sbase, const int* cs, const M* vs) {
+        constexpr bool FAST = decltype(fast_tag)::value;
+        const int lane = static_cast<int>(r & 31);
+        int coff, w;
+        if constexpr (FAST) {
+            coff = static_cast<int>((r >> 5) - c0) * (32 * MAXW) + lane;
+            w = MAXW;
+        } else {
+            const int64_t chunk = r >> 5;
+            const int64_t cb = __ldg(&cptr[chunk]);
+            coff = static_cast<int>(cb - sbase) + lane;
+            w = static_cast<int>((__ldg(&cptr[chunk + 1]) - cb) >> 5);
+        }
+        const int64_t own = r * pitch;
+        T wi{}, xi{}, x0v{};
+        if constexpr (KIND == kStepFused || KIND == kStepRecur) wi = ld_stream(&W[own]);
+        if constexpr (KIND == kStepFused || KIND == kStepStart2) xi = ld_stream(&X[own]);
+        if constexpr (DMODE == 2 && KIND != kStepStart2) x0v = ld_stream(&X0[own]);
+        T acc = O::zero();
+        if constexpr (FAST) {
+            int c[MAXW];
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j) c[j] = cs[coff + j * 32];
+            T g[MAXW];
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j) g[j] = ldg(&inu[static_cast<int64_t>(c[j]) * pitch]);
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j) acc = O::vadd(acc, O::prod(vs[coff + j * 32], g[j]));
+        } else {
+            int c[MAXW];
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j) c[j] = (j < w) ? cs[coff + j * 32] : -1;
+            T g[MAXW];
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j)
+                if (c[j] >= 0) g[j] = ldg(&inu[static_cast<int64_t>(c[j]) * pitch]);
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j)
+                if (c[j] >= 0) acc = O::vadd(acc, O::prod(vs[coff + j * 32], g[j]));
+        }
+        const T ui = ldg(&inu[(r + halo) * pitch]);
+        step_epilogue<O, T, KIND, DMODE>(acc, ui, wi, xi, x0v, own, W, X, X0, p.beta, coeff, c1,
+                                         c2, acc_d, comp_d);
+    };
+
     if (t == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -496,41 +544,26 @@ __global__ void __launch_bounds__(256, 2) step_tma_kernel(const StepParams p) {
     for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
         const int buf = k & 1;
         if (t == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
+        const int64_t c0 = cbeg + tile * NCH;
+        const int64_t c1e = min(c0 + NCH, cend);
+        const int64_t sbase = cptr[c0];
+        // fast tile: all chunks full, width == MAXW, tile fully inside [row0, row1)
+        bool fast = (cptr[c1e] - sbase) == (c1e - c0) * 32 * MAXW && c0 * 32 >= row0 &&
+                    c1e * 32 <= row1 && (c1e - c0) == NCH;
+        for (int64_t c = c0; fast && c < c1e; ++c) fast = __ldg(&p.chunk_full[c]) != 0;
         mbar_wait(&bars[buf], (phases >> buf) & 1u);
         phases ^= 1u << buf;
-        const int64_t c0 = cbeg + tile * NCH;
-        const int64_t sbase = cptr[c0];
         const int* cs = cols_s + buf * cap;
         const M* vs = vals_s + buf * cap;
-        for (int it = 0; it < TR; it += R) {
-            const int64_t r = c0 * 32 + it + rr;
-            if (r < row0 || r >= row1) continue;
-            const int64_t chunk = r >> 5;
-            const int lane = static_cast<int>(r & 31);
-            const int coff = static_cast<int>(__ldg(&cptr[chunk]) - sbase) + lane;
-            const int w = static_cast<int>((__ldg(&cptr[chunk + 1]) - __ldg(&cptr[chunk])) >> 5);
-            const int64_t own = r * pitch;
-            T wi{}, xi{}, x0v{};
-            if constexpr (KIND == kStepFused || KIND == kStepRecur) wi = ld_stream(&W[own]);
-            if constexpr (KIND == kStepFused || KIND == kStepStart2) xi = ld_stream(&X[own]);
-            if constexpr (DMODE == 2 && KIND != kStepStart2) x0v = ld_stream(&X0[own]);
-            int c[MAXW];
-#pragma unroll
-            for (int j = 0; j < MAXW; ++j) c[j] = (j < w) ? cs[coff + j * 32] : -1;
-            T g[MAXW];
-#pragma unroll
-            for (int j = 0; j < MAXW; ++j)
-                if (c[j] >= 0) g[j] = ldg(&inu[static_cast<int64_t>(c[j]) * pitch]);
-            const T ui = ldg(&inu[(r + halo) * pitch]);
-            T acc = O::zero();
-#pragma unroll
-            for (int j = 0; j < MAXW; ++j)
-                if (c[j] >= 0) {
-                    const M v = vs[coff + j * 32];
-                    acc = O::vadd(acc, O::prod(PRESCALED ? v : O::scale(v, alpha), g[j]));
-                }
-            step_epilogue<O, T, KIND, DMODE>(acc, ui, wi, xi, x0v, own, W, X, X0, p.beta, coeff,
-                                             c1, c2, acc_d, comp_d);
+        if (fast) {
+            for (int it = 0; it < TR; it += R)
+                row(std::true_type{}, c0 * 32 + it + rr, c0, sbase, cs, vs);
+        } else {
+            for (int it = 0; it < TR; it += R) {
+                const int64_t r = c0 * 32 + it + rr;
+                if (r < row0 || r >= row1) continue;
+                row(std::false_type{}, r, c0, sbase, cs, vs);
+            }
         }
         __syncthreads();  // buffer `buf` is refilled two tiles later
     }
@@ -660,15 +693,19 @@ __global__ void philox_normal_kernel(double* __restrict__ x, int64_t n, uint64_t
 
 // ---- SELL build --------------------------------------------------------------------------
 __global__ void sell_width_kernel(const int64_t* __restrict__ offs, int64_t rows, int64_t nchunks,
-                                  int64_t* __restrict__ slots, int* __restrict__ maxlen) {
+                                  int64_t* __restrict__ slots, int* __restrict__ maxlen,
+                                  unsigned char* __restrict__ full) {
     const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (c >= nchunks) return;
-    int64_t w = 0;
+    int64_t w = 0, wmin = INT64_MAX;
     for (int l = 0; l < kChunk; ++l) {
         const int64_t r = c * kChunk + l;
-        if (r < rows) w = max(w, offs[r + 1] - offs[r]);
+        const int64_t len = r < rows ? offs[r + 1] - offs[r] : -1;
+        w = max(w, len);
+        wmin = min(wmin, len);
     }
     slots[c] = w * kChunk;
+    full[c] = (wmin == w) ? 1 : 0;  // no padding slot anywhere in the chunk
     atomicMax(maxlen, static_cast<int>(w));
 }
 
@@ -754,11 +791,10 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
     const int64_t nrows = s.row1 - s.row0;
     constexpr int MW = MAXW > 0 ? MAXW : 4;
-    const bool tma = MAXW > 0 && ctx.kernel_variant == 1;
-    const void* svals = tma ? find_scaled(a, s.alpha) : nullptr;
-    auto kernel = tma ? (svals ? step_tma_kernel<CPLX, T, KIND, DMODE, MW, true>
-                               : step_tma_kernel<CPLX, T, KIND, DMODE, MW, false>)
-                      : step_kernel<CPLX, T, KIND, DMODE, MAXW>;
+    const void* svals = s.alpha == 1.0 ? a.vals.p : find_scaled(a, s.alpha);
+    const bool tma = MAXW > 0 && ctx.kernel_variant == 1 && svals != nullptr;
+    auto kernel = tma ? step_tma_kernel<CPLX, T, KIND, DMODE, MW>
+                      : step_kernel<CPLX, T, KIND, DMODE, 0>;
     int used_total = 0;
     // column slabs of at most 256 units (one CTA row-group spans a slab)
     for (int u0 = 0; u0 < units; u0 += 256) {
@@ -794,6 +830,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, maxb)));
         StepParams p{};
         p.chunk_ptr = a.chunk_ptr.as<int64_t>();
+        p.chunk_full = a.chunk_full.as<unsigned char>();
         p.cols = a.cols.as<int>();
         p.vals = a.vals.p;
         p.svals = svals;
@@ -866,7 +903,8 @@ template <bool CPLX, class T>
 void dispatch_kind(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
     const int w = s.a->max_row_len;
     if (w <= 4) return dispatch_kind_w<CPLX, T, 4>(ctx, s, st, units, pitch);
-    if (w <= 12) return dispatch_kind_w<CPLX, T, 12>(ctx, s, st, units, pitch);
+    if (w <= 8) return dispatch_kind_w<CPLX, T, 8>(ctx, s, st, units, pitch);
+    if (w <= 11) return dispatch_kind_w<CPLX, T, 11>(ctx, s, st, units, pitch);
     if (w <= 16) return dispatch_kind_w<CPLX, T, 16>(ctx, s, st, units, pitch);
     return dispatch_kind_w<CPLX, T, 0>(ctx, s, st, units, pitch);
 }
@@ -1010,12 +1048,14 @@ void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d
     m.nchunks = (rows + kChunk - 1) / kChunk;
     m.chunk_ptr.ensure(sizeof(int64_t) * (m.nchunks + 1));
     DeviceBuffer slots(sizeof(int64_t) * (m.nchunks + 1));
+    m.chunk_full.ensure(static_cast<size_t>(m.nchunks) + 16);
     DeviceBuffer dmax(sizeof(int) * 2);
     CFD_CUDA(cudaMemsetAsync(dmax.p, 0, sizeof(int) * 2, st));
     CFD_CUDA(cudaMemsetAsync(slots.p, 0, sizeof(int64_t) * (m.nchunks + 1), st));
     if (m.nchunks > 0) {
         sell_width_kernel<<<static_cast<unsigned>((m.nchunks + 255) / 256), 256, 0, st>>>(
-            d_offs, rows, m.nchunks, slots.as<int64_t>(), dmax.as<int>());
+            d_offs, rows, m.nchunks, slots.as<int64_t>(), dmax.as<int>(),
+            m.chunk_full.as<unsigned char>());
         CFD_CUDA(cudaGetLastError());
     }
     size_t tmp_bytes = 0;
