@@ -112,6 +112,30 @@ int chebfd_csr_topological_insulator(const chebfd_lattice* spec, int64_t row_beg
                                      int64_t row_end, int64_t* dim, int64_t* nnz, int64_t* offs,
                                      int64_t* cols, void* vals);
 
+/* ---- distributed row partition (host-only planning) --------------------------- */
+/* One process per GPU: contiguous row ranges on lattice planes (TI z-planes,
+ * graphene y-rows); gathered blocks live in an extended row space
+ * [halo_lo | owned | halo_hi].  The reference has no distribution; this
+ * restates the paper's GHOST row distribution. */
+typedef struct {
+    int64_t dim, row_begin, local_rows;
+    int64_t halo_lo, halo_hi;           /* rows received from lo / hi neighbour */
+    int64_t lo_src_begin, hi_src_begin; /* first global row of each halo */
+    int lo_rank, hi_rank;               /* -1: none */
+    int64_t bnd_lo, bnd_hi;             /* rows [0,bnd_lo) / last bnd_hi read a halo */
+    int64_t send_lo_begin, send_lo_n;   /* local rows sent to lo_rank */
+    int64_t send_hi_begin, send_hi_n;   /* local rows sent to hi_rank */
+} chebfd_partition;
+/* Plan rank `rank` of `nranks` for a lattice model (0 graphene, 1 TI): rows
+ * and halos; send ranges stay zero until chebfd_plan_sends. */
+int chebfd_plan_partition(const chebfd_lattice* spec, int model, int rank, int nranks,
+                          chebfd_partition* out);
+/* Fill the send ranges from every rank's (halo_lo, halo_hi, lo_rank, hi_rank),
+ * all4[4*nranks] (what the device path all-gathers over NCCL). */
+int chebfd_plan_sends(chebfd_partition* p, int rank, int nranks, const int64_t* all4);
+/* Extended-row index of global column g, or -2 if this rank holds no copy. */
+int64_t chebfd_plan_map_column(const chebfd_partition* p, int64_t g);
+
 /* ---- device sparse matrix (SELL-C-sigma, C = 32, sigma = 1) ----------------- */
 /* From a full host CSR (SparseMatrix ctor + validate, sparse_matrix.hpp:22-100).
  * In a distributed context every rank passes the full matrix and keeps its

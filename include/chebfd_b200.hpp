@@ -1,0 +1,393 @@
+// chebfd_b200.hpp -- the reference's C++ driver API, backed by the sm_100a
+// library through the C ABI in chebfd_b200.h.
+//
+// A caller of /root/reference/proj/include/chebfd/*.hpp switches by
+// replacing `chebfd::` with `chebfd::b200::` and passing a Context: the
+// template signatures (double / std::complex<double>), argument meaning,
+// return types and exception types (std::invalid_argument,
+// std::runtime_error, std::domain_error, std::out_of_range) are the
+// reference's.  Sparse matrices and block vectors live on the GPU; upload /
+// download move row-major host data (block_vector.hpp:15-16).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "chebfd_b200.h"
+
+namespace chebfd::b200 {
+
+using Index = std::int64_t;
+using Complex = std::complex<double>;
+
+template <class S>
+inline constexpr int kind_of = std::is_same_v<S, Complex> ? CHEBFD_COMPLEX128 : CHEBFD_REAL64;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+    if (rc == CHEBFD_OK) return;
+    const std::string m = chebfd_last_error();
+    switch (rc) {
+        case CHEBFD_ERR_INVALID_ARGUMENT: throw std::invalid_argument(m);
+        case CHEBFD_ERR_DOMAIN: throw std::domain_error(m);
+        case CHEBFD_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
+        case CHEBFD_ERR_CUDA:
+        case CHEBFD_ERR_NCCL: throw CudaError(m);
+        default: throw std::runtime_error(m);
+    }
+}
+
+// ---- context (replaces the OpenMP runtime, parallel.hpp) ---------------------------
+class Context {
+  public:
+    explicit Context(int device = 0) { check(chebfd_ctx_create(device, &h_)); }
+    Context(int device, int rank, int nranks, const unsigned char id[128]) {
+        check(chebfd_ctx_create_dist(device, rank, nranks, id, &h_));
+    }
+    ~Context() {
+        if (h_) chebfd_ctx_destroy(h_);
+    }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    chebfd_ctx* get() const { return h_; }
+    void synchronize() { check(chebfd_ctx_synchronize(h_)); }
+
+  private:
+    chebfd_ctx* h_ = nullptr;
+};
+
+// ---- intervals, kernels, lattice (filter.hpp, models.hpp) ---------------------------
+struct Interval {
+    double lo = 0.0, hi = 0.0;
+    double width() const { return hi - lo; }
+    double half_width() const { return 0.5 * (hi - lo); }
+    double center() const { return 0.5 * (lo + hi); }
+    bool contains(double x) const { return x >= lo && x <= hi; }
+    bool contains(const Interval& o) const { return lo <= o.lo && o.hi <= hi; }
+};
+
+enum class KernelKind { None = CHEBFD_KERNEL_NONE, Fejer = CHEBFD_KERNEL_FEJER,
+                        Jackson = CHEBFD_KERNEL_JACKSON, Lanczos = CHEBFD_KERNEL_LANCZOS };
+struct Kernel {
+    KernelKind kind = KernelKind::Lanczos;
+    int mu = 2;
+};
+
+enum class Boundary { periodic_xy_open_z = CHEBFD_PERIODIC_XY_OPEN_Z,
+                      periodic_all = CHEBFD_PERIODIC_ALL, open_all = CHEBFD_OPEN_ALL };
+struct LatticeSpec {
+    Index lx = 1, ly = 1, lz = 1;
+    double t = 1.0;
+    double disorder = 0.0;
+    Boundary boundary = Boundary::periodic_xy_open_z;
+    std::uint64_t seed = 1;
+    chebfd_lattice c() const {
+        return {lx, ly, lz, t, disorder, static_cast<int>(boundary), seed};
+    }
+};
+
+// ---- device sparse matrix (SELL-C-sigma) -----------------------------------------------
+template <class S>
+class SparseMatrix {
+  public:
+    SparseMatrix(Context& ctx, Index dim, const std::vector<Index>& row_offsets,
+                 const std::vector<Index>& col_indices, const std::vector<S>& values) {
+        if (static_cast<Index>(row_offsets.size()) != dim + 1)
+            throw std::invalid_argument("SparseMatrix: row_offsets length must be dim+1");
+        if (col_indices.size() != values.size())
+            throw std::invalid_argument("SparseMatrix: col/value length mismatch");
+        chebfd_matrix* h = nullptr;
+        check(chebfd_matrix_from_csr(ctx.get(), kind_of<S>, dim, row_offsets.data(),
+                                     col_indices.data(), values.data(), &h));
+        h_.reset(h);
+    }
+    explicit SparseMatrix(chebfd_matrix* h) : h_(h) {}
+    Index dim() const { return info().dim; }
+    Index nnz() const { return info().nnz; }
+    double avg_nonzeros_per_row() const { return dim() ? double(nnz()) / double(dim()) : 0.0; }
+    chebfd_matrix_info info() const {
+        chebfd_matrix_info i{};
+        check(chebfd_matrix_get_info(h_.get(), &i));
+        return i;
+    }
+    chebfd_matrix* get() const { return h_.get(); }
+
+  private:
+    struct Del {
+        void operator()(chebfd_matrix* m) const { chebfd_matrix_destroy(m); }
+    };
+    std::unique_ptr<chebfd_matrix, Del> h_;
+};
+
+inline SparseMatrix<double> graphene(Context& ctx, const LatticeSpec& s) {
+    chebfd_matrix* h = nullptr;
+    const chebfd_lattice l = s.c();
+    check(chebfd_matrix_graphene(ctx.get(), &l, &h));
+    return SparseMatrix<double>(h);
+}
+
+inline SparseMatrix<Complex> topological_insulator(Context& ctx, const LatticeSpec& s) {
+    chebfd_matrix* h = nullptr;
+    const chebfd_lattice l = s.c();
+    check(chebfd_matrix_topological_insulator(ctx.get(), &l, &h));
+    return SparseMatrix<Complex>(h);
+}
+
+// ---- device block vector -----------------------------------------------------------------
+template <class S>
+class BlockVector {
+  public:
+    BlockVector(const SparseMatrix<S>& a, Index width) {
+        chebfd_block* h = nullptr;
+        check(chebfd_block_create(a.get(), width, &h));
+        h_.reset(h);
+    }
+    explicit BlockVector(chebfd_block* h) : h_(h) {}
+    Index dim() const { return info(1); }
+    Index width() const { return info(2); }
+    void upload(const std::vector<S>& host) {
+        if (static_cast<Index>(host.size()) != dim() * width())
+            throw std::invalid_argument("BlockVector::upload: size mismatch");
+        check(chebfd_block_upload(h_.get(), host.data()));
+    }
+    std::vector<S> download() const {
+        std::vector<S> out(static_cast<size_t>(dim() * width()));
+        check(chebfd_block_download(h_.get(), out.data()));
+        return out;
+    }
+    void randomize(std::uint64_t seed) { check(chebfd_block_randomize(h_.get(), seed)); }
+    chebfd_block* get() const { return h_.get(); }
+
+  private:
+    Index info(int what) const {
+        int k = 0;
+        int64_t r = 0, w = 0, b = 0;
+        check(chebfd_block_info(h_.get(), &k, &r, &w, &b));
+        return what == 1 ? r : w;
+    }
+    struct Del {
+        void operator()(chebfd_block* b) const { chebfd_block_destroy(b); }
+    };
+    std::unique_ptr<chebfd_block, Del> h_;
+};
+
+template <class S>
+struct DenseMatrix {
+    Index rows = 0, cols = 0;
+    std::vector<S> a;
+    DenseMatrix() = default;
+    DenseMatrix(Index r, Index c) : rows(r), cols(c), a(static_cast<size_t>(r * c), S{}) {}
+    S& operator()(Index i, Index j) { return a[static_cast<size_t>(i * cols + j)]; }
+    const S& operator()(Index i, Index j) const { return a[static_cast<size_t>(i * cols + j)]; }
+};
+
+// ---- kernels (kernels.hpp) ------------------------------------------------------------------
+template <class S>
+BlockVector<S> spmmvm(const SparseMatrix<S>& A, const BlockVector<S>& X, double alpha, double beta) {
+    BlockVector<S> Y(A, X.width());
+    check(chebfd_spmmvm(A.get(), X.get(), Y.get(), alpha, beta));
+    return Y;
+}
+
+template <class S>
+void spmmvm_fused(const SparseMatrix<S>& A, const BlockVector<S>& U, BlockVector<S>& W,
+                  BlockVector<S>& X, double alpha, double beta, double coeff, S* dots = nullptr) {
+    check(chebfd_spmmvm_fused(A.get(), U.get(), W.get(), X.get(), alpha, beta, coeff, dots));
+}
+
+template <class S>
+void recurrence_step(const SparseMatrix<S>& A, const BlockVector<S>& U, BlockVector<S>& W,
+                     double alpha, double beta) {
+    check(chebfd_recurrence_step(A.get(), U.get(), W.get(), alpha, beta));
+}
+
+template <class S>
+void block_axpy_scal(BlockVector<S>& X, const BlockVector<S>& U, const BlockVector<S>& W,
+                     double c0, double c1, double c2) {
+    check(chebfd_block_axpy_scal(X.get(), U.get(), W.get(), c0, c1, c2));
+}
+
+template <class S>
+DenseMatrix<S> gram(const BlockVector<S>& X, const BlockVector<S>& Y) {
+    DenseMatrix<S> G(X.width(), Y.width());
+    check(chebfd_gram(X.get(), Y.get(), G.a.data()));
+    return G;
+}
+
+template <class S>
+std::vector<S> column_dots(const BlockVector<S>& X, const BlockVector<S>& Y) {
+    std::vector<S> d(static_cast<size_t>(X.width()));
+    check(chebfd_column_dots(X.get(), Y.get(), d.data()));
+    return d;
+}
+
+template <class S>
+std::vector<double> column_norms(const BlockVector<S>& X) {
+    std::vector<double> n(static_cast<size_t>(X.width()));
+    check(chebfd_column_norms(X.get(), n.data()));
+    return n;
+}
+
+template <class S>
+BlockVector<S> block_mult_small(const SparseMatrix<S>& A, const BlockVector<S>& X,
+                                const DenseMatrix<S>& B) {
+    if (X.width() != B.rows) throw std::invalid_argument("block_mult_small: shape mismatch");
+    BlockVector<S> Y(A, B.cols);
+    check(chebfd_block_mult_small(X.get(), B.a.data(), B.cols, Y.get()));
+    return Y;
+}
+
+// ---- filter (filter.hpp) -----------------------------------------------------------------------
+struct FilterPolynomial {
+    int degree = 0;
+    std::vector<double> combined;
+    double alpha = 1.0, beta = 0.0;
+    Interval target, bounds;
+    Kernel kernel;
+};
+
+inline std::vector<double> window_coeffs(Interval target, Interval bounds, int degree) {
+    std::vector<double> c(static_cast<size_t>(degree < 0 ? 0 : degree) + 1);
+    check(chebfd_window_coeffs(target.lo, target.hi, bounds.lo, bounds.hi, degree, c.data()));
+    return c;
+}
+
+inline std::vector<double> kernel_coeffs(Kernel k, int degree) {
+    std::vector<double> g(static_cast<size_t>(degree < 0 ? 0 : degree) + 1);
+    check(chebfd_kernel_coeffs(static_cast<int>(k.kind), k.mu, degree, g.data()));
+    return g;
+}
+
+inline FilterPolynomial make_filter(Interval target, Interval bounds, int degree, Kernel kernel) {
+    FilterPolynomial p;
+    p.degree = degree;
+    p.target = target;
+    p.bounds = bounds;
+    p.kernel = kernel;
+    p.combined.resize(static_cast<size_t>(degree < 0 ? 0 : degree) + 1);
+    check(chebfd_make_filter(target.lo, target.hi, bounds.lo, bounds.hi, degree,
+                             static_cast<int>(kernel.kind), kernel.mu, p.combined.data(), &p.alpha,
+                             &p.beta));
+    return p;
+}
+
+inline double eval_scalar(const FilterPolynomial& p, double x) {
+    double out = 0.0;
+    check(chebfd_eval_scalar(p.combined.data(), p.degree, p.alpha, p.beta, p.bounds.lo, p.bounds.hi,
+                             x, &out));
+    return out;
+}
+
+struct MomentTable {
+    Index degree = 0, width = 0;
+    std::vector<double> m;
+    double& operator()(Index n, Index k) { return m[static_cast<size_t>(n * width + k)]; }
+    double operator()(Index n, Index k) const { return m[static_cast<size_t>(n * width + k)]; }
+};
+
+template <class S>
+std::optional<MomentTable> apply_filter(const SparseMatrix<S>& A, BlockVector<S>& X,
+                                        const FilterPolynomial& p, bool want_moments = false) {
+    std::optional<MomentTable> mt;
+    if (want_moments) {
+        mt = MomentTable{p.degree, X.width(),
+                         std::vector<double>(static_cast<size_t>((p.degree + 1) * X.width()))};
+    }
+    check(chebfd_apply_filter(A.get(), X.get(), p.combined.data(), p.degree, p.alpha, p.beta,
+                              mt ? mt->m.data() : nullptr));
+    return mt;
+}
+
+// ---- solver / spectral (solver.hpp, spectral.hpp) ------------------------------------------------
+inline Interval lanczos_bounds_of(chebfd_matrix* a, int iters, std::uint64_t seed) {
+    Interval b;
+    check(chebfd_lanczos_bounds(a, iters, seed, &b.lo, &b.hi));
+    return b;
+}
+
+template <class S>
+Interval lanczos_bounds(const SparseMatrix<S>& A, int iters, std::uint64_t seed = 1) {
+    return lanczos_bounds_of(A.get(), iters, seed);
+}
+
+struct SolverOptions {
+    Interval target;
+    double epsilon = 1e-10;
+    int n_search = 0;
+    int degree = 0;
+    Kernel kernel{KernelKind::Lanczos, 2};
+    int max_iters = 40;
+    std::uint64_t seed = 1;
+    int dos_moments = 2000;
+    int dos_samples = 32;
+    bool deterministic = true;
+    Interval bounds{0.0, 0.0};
+    bool collect_weight_density = true;
+};
+
+struct ConvergenceReport {
+    bool converged = false;
+    int iterations = 0;
+    double total_spmvms = 0.0;
+    int n_search = 0, degree = 0;
+    double sigma = 0.0, eta = 0.0;
+    Interval bounds;
+    double matrix_norm_est = 0.0, n_target_estimate = 0.0;
+    std::vector<double> values, residual_norms;
+    std::vector<bool> accepted;
+    double weight_integral = 0.0, seconds = 0.0;
+};
+
+template <class S>
+ConvergenceReport solve(const SparseMatrix<S>& A, const SolverOptions& o) {
+    chebfd_solver_options c{};
+    chebfd_solver_options_default(&c);
+    c.target_lo = o.target.lo;
+    c.target_hi = o.target.hi;
+    c.epsilon = o.epsilon;
+    c.n_search = o.n_search;
+    c.degree = o.degree;
+    c.kernel = static_cast<int>(o.kernel.kind);
+    c.kernel_mu = o.kernel.mu;
+    c.max_iters = o.max_iters;
+    c.seed = o.seed;
+    c.dos_moments = o.dos_moments;
+    c.dos_samples = o.dos_samples;
+    c.bounds_lo = o.bounds.lo;
+    c.bounds_hi = o.bounds.hi;
+    c.collect_weight_density = o.collect_weight_density ? 1 : 0;
+    chebfd_solve_report r{};
+    const int cap = 4096 + 2 * o.n_search;
+    std::vector<double> vals(cap), res(cap);
+    std::vector<int> acc(cap);
+    check(chebfd_solve(A.get(), &c, &r, cap, vals.data(), res.data(), acc.data(), nullptr, nullptr));
+    ConvergenceReport out;
+    out.converged = r.converged != 0;
+    out.iterations = r.iterations;
+    out.total_spmvms = r.total_spmvms;
+    out.n_search = r.n_search;
+    out.degree = r.degree;
+    out.sigma = r.sigma;
+    out.eta = r.eta;
+    out.bounds = {r.bounds_lo, r.bounds_hi};
+    out.matrix_norm_est = r.matrix_norm_est;
+    out.n_target_estimate = r.n_target_estimate;
+    out.values.assign(vals.begin(), vals.begin() + r.n_values);
+    out.residual_norms.assign(res.begin(), res.begin() + r.n_values);
+    for (int k = 0; k < r.n_values; ++k) out.accepted.push_back(acc[k] != 0);
+    out.weight_integral = r.weight_integral;
+    out.seconds = r.seconds;
+    return out;
+}
+
+}  // namespace chebfd::b200

@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     apply_filter, apply_filter_host, block_axpy_scal, block_mult_small, column_dots, column_norms,
     csr_graphene, csr_topological_insulator, estimate_count, eval_scalar, gram, intensity_model,
     kernel_coeffs, kpm_dos, lanczos_bounds, make_filter, per_row_bytes, per_row_flops,
+    plan_all4, plan_complete_sends, plan_map_column, plan_partition, plan_sends,
     rayleigh_ritz, recurrence_step, solve, spmmvm, spmmvm_fused, svqb_orthonormalize,
     window_coeffs,
 )

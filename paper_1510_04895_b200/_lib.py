@@ -25,6 +25,14 @@ class chebfd_lattice(C.Structure):
                 ("boundary", _int), ("seed", _u64)]
 
 
+class chebfd_partition(C.Structure):
+    _fields_ = [("dim", _i64), ("row_begin", _i64), ("local_rows", _i64), ("halo_lo", _i64),
+                ("halo_hi", _i64), ("lo_src_begin", _i64), ("hi_src_begin", _i64),
+                ("lo_rank", _int), ("hi_rank", _int), ("bnd_lo", _i64), ("bnd_hi", _i64),
+                ("send_lo_begin", _i64), ("send_lo_n", _i64), ("send_hi_begin", _i64),
+                ("send_hi_n", _i64)]
+
+
 class chebfd_matrix_info(C.Structure):
     _fields_ = [("kind", _int), ("dim", _i64), ("nnz", _i64), ("local_rows", _i64),
                 ("row_begin", _i64), ("local_nnz", _i64), ("sell_entries", _i64),
@@ -63,6 +71,9 @@ _SIGS = {
     "chebfd_host_free": (_int, [_vp]),
     "chebfd_csr_graphene": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "chebfd_csr_topological_insulator": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "chebfd_plan_partition": (_int, [_vp, _int, _int, _int, _vp]),
+    "chebfd_plan_sends": (_int, [_vp, _int, _int, _vp]),
+    "chebfd_plan_map_column": (_i64, [_vp, _i64]),
     "chebfd_matrix_from_csr": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _pp]),
     "chebfd_matrix_graphene": (_int, [_vp, _vp, _pp]),
     "chebfd_matrix_topological_insulator": (_int, [_vp, _vp, _pp]),

@@ -740,3 +740,37 @@ def intensity_model(n_nzr, s_d, s_i, f_a, f_m, n_b):
     if not n_nzr > 0:
         raise InvalidArgument("intensity_model: N_nzr must be positive")
     return per_row_flops(n_nzr, f_a, f_m) / per_row_bytes(n_nzr, s_d, s_i, n_b)
+
+
+# ------------------------------------------------- distributed planning --
+def plan_partition(spec: LatticeSpec, model: str, rank: int, nranks: int):
+    """Rows and halos of `rank` for a lattice model ("graphene" | "ti"),
+    partitioned on lattice planes; send ranges via plan_complete_sends."""
+    out = L.chebfd_partition()
+    s = spec._c()
+    _check(_lib().chebfd_plan_partition(C.byref(s), {"graphene": 0, "ti": 1}[model], rank, nranks,
+                                        C.byref(out)))
+    return out
+
+
+def plan_all4(plan) -> list:
+    """This rank's (halo_lo, halo_hi, lo_rank, hi_rank) -- what ranks all-gather."""
+    return [plan.halo_lo, plan.halo_hi, plan.lo_rank, plan.hi_rank]
+
+
+def plan_sends(plan, rank: int, all4) -> None:
+    """Fill plan's send ranges from every rank's plan_all4 (flattened)."""
+    arr = np.ascontiguousarray(np.asarray(all4, dtype=np.int64).reshape(-1))
+    _check(_lib().chebfd_plan_sends(C.byref(plan), rank, len(arr) // 4, _ptr(arr)))
+
+
+def plan_complete_sends(plans) -> None:
+    """Single-process helper: complete the send ranges of all ranks' plans."""
+    all4 = [v for p in plans for v in plan_all4(p)]
+    for r, p in enumerate(plans):
+        plan_sends(p, r, all4)
+
+
+def plan_map_column(plan, g: int) -> int:
+    """Extended-row index of global column g on this rank (-2: not held)."""
+    return int(_lib().chebfd_plan_map_column(C.byref(plan), int(g)))

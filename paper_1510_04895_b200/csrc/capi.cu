@@ -251,58 +251,9 @@ void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
 // neighbours need from it.
 void setup_partition(Context& c, Matrix& m, const HostCsr& csr, int64_t r0, int64_t r1,
                      const std::vector<int64_t>& starts) {
+    m.part = plan_rows(csr, r0, r1, starts);
     Partition& p = m.part;
-    p.dim = csr.dim;
-    p.row_begin = r0;
-    p.local = r1 - r0;
-    const int64_t D = csr.dim;
-    int64_t max_up = -1, max_dn = -1;
-    int64_t bnd_lo = 0, bnd_hi = 0;
-    for (int64_t i = 0; i < p.local; ++i) {
-        bool lo_ref = false, hi_ref = false;
-        for (int64_t q = csr.offs[i]; q < csr.offs[i + 1]; ++q) {
-            const int64_t g = csr.cols[q];
-            if (g >= r0 && g < r1) continue;
-            const int64_t up = ((g - r1) % D + D) % D;
-            const int64_t dn = ((r0 - 1 - g) % D + D) % D;
-            if (up <= dn) {
-                max_up = std::max(max_up, up);
-                hi_ref = true;
-            } else {
-                max_dn = std::max(max_dn, dn);
-                lo_ref = true;
-            }
-        }
-        if (lo_ref) bnd_lo = i + 1;
-        if (hi_ref) bnd_hi = std::max(bnd_hi, p.local - i);
-    }
     const int P = c.nranks;
-    auto owner = [&](int64_t g) {
-        return static_cast<int>(std::upper_bound(starts.begin(), starts.end(), g) - starts.begin()) - 1;
-    };
-    if (max_up >= 0) {
-        p.halo_hi = max_up + 1;
-        p.hi_src_begin = r1 % D;
-        p.hi_rank = owner(p.hi_src_begin);
-        const int64_t hi_end = starts[p.hi_rank + 1];
-        if (p.hi_src_begin + p.halo_hi > hi_end)
-            fail(CHEBFD_ERR_UNSUPPORTED, "upper halo spans more than one neighbour rank");
-    }
-    if (max_dn >= 0) {
-        p.halo_lo = max_dn + 1;
-        const int64_t lo_end = r0 == 0 ? D : r0;
-        p.lo_src_begin = lo_end - p.halo_lo;
-        p.lo_rank = owner(lo_end - 1);
-        if (p.lo_src_begin < starts[p.lo_rank])
-            fail(CHEBFD_ERR_UNSUPPORTED, "lower halo spans more than one neighbour rank");
-    }
-    // bnd_hi counted as distance from the end
-    p.bnd_lo = bnd_lo;
-    p.bnd_hi = bnd_hi;
-    if (p.bnd_lo + p.bnd_hi > p.local) {  // tiny partitions: everything is boundary
-        p.bnd_lo = p.local;
-        p.bnd_hi = 0;
-    }
     // what do the neighbours need from me?  all-gather (halo_lo, halo_hi, lo_rank, hi_rank)
     std::vector<int64_t> mine = {p.halo_lo, p.halo_hi, p.lo_rank, p.hi_rank};
     std::vector<int64_t> all(4 * P, 0);
@@ -315,33 +266,10 @@ void setup_partition(Context& c, Matrix& m, const HostCsr& csr, int64_t r0, int6
         CFD_CUDA(cudaMemcpyAsync(all.data(), d.p, sizeof(int64_t) * 4 * P, cudaMemcpyDeviceToHost,
                                  c.stream));
         ctx_sync(c);
+    } else {
+        all = mine;
     }
-    // my hi neighbour's lo halo are my LAST rows; my lo neighbour's hi halo my FIRST rows
-    if (p.hi_rank >= 0 && P > 1) {
-        const int64_t need = all[4 * p.hi_rank + 0];
-        if (all[4 * p.hi_rank + 2] == c.rank && need > 0) {
-            p.send_hi_n = need;
-            p.send_hi_begin = p.local - need;
-        }
-    }
-    if (p.lo_rank >= 0 && P > 1) {
-        const int64_t need = all[4 * p.lo_rank + 1];
-        if (all[4 * p.lo_rank + 3] == c.rank && need > 0) {
-            p.send_lo_n = need;
-            p.send_lo_begin = 0;
-        }
-    }
-    // a neighbour that needs rows from me although I do not read from it
-    // (asymmetric stencils) is not supported by the symmetric protocol
-    for (int q = 0; q < P; ++q) {
-        if (q == c.rank) continue;
-        if (all[4 * q + 2] == c.rank && all[4 * q + 0] > 0 && p.hi_rank != q)
-            fail(CHEBFD_ERR_UNSUPPORTED, "asymmetric halo pattern");
-        if (all[4 * q + 3] == c.rank && all[4 * q + 1] > 0 && p.lo_rank != q)
-            fail(CHEBFD_ERR_UNSUPPORTED, "asymmetric halo pattern");
-    }
-    if (p.send_lo_n > p.local || p.send_hi_n > p.local)
-        fail(CHEBFD_ERR_UNSUPPORTED, "neighbour halo larger than this rank's rows");
+    plan_sends(p, c.rank, P, all.data());
 }
 
 std::unique_ptr<Matrix> matrix_from_host_csr(Context& c, const HostCsr& csr, int64_t r0, int64_t r1,
@@ -383,15 +311,8 @@ int64_t allreduce_count(Context& c, int64_t v) {
 
 std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool ti) {
     validate_lattice(s, ti);
-    const int64_t dim = ti ? 4 * s.lx * s.ly * s.lz : 2 * s.lx * s.ly;
-    const int64_t plane = ti ? 4 * s.lx * s.ly : 2 * s.lx;  // TI z-plane / graphene y-row
-    std::vector<int64_t> starts(c.nranks + 1);
-    for (int q = 0; q < c.nranks; ++q) {
-        int64_t a, b;
-        plane_partition(dim, plane, q, c.nranks, &a, &b);
-        starts[q] = a;
-        starts[q + 1] = b;
-    }
+    std::vector<int64_t> starts;
+    lattice_starts(s, ti, c.nranks, starts);
     const int64_t r0 = starts[c.rank], r1 = starts[c.rank + 1];
     HostCsr csr = ti ? gen_topological_insulator(s, r0, r1) : gen_graphene(s, r0, r1);
     const int64_t nnz_g = allreduce_count(c, static_cast<int64_t>(csr.cols.size()));

@@ -64,6 +64,26 @@ struct Partition {
     int64_t ext_rows() const { return halo_lo + local + halo_hi; }
 };
 
+// Extended-row index of global column g in a partition (-2: not held).  Used
+// by the SELL builder on the device and by the host planning API.
+#ifdef __CUDACC__
+#define CFD_HD __host__ __device__
+#else
+#define CFD_HD
+#endif
+struct ColMap {
+    int64_t row_begin, local, halo_lo, halo_hi, lo_src, hi_src;
+    CFD_HD int64_t map(int64_t g) const {
+        if (g >= row_begin && g < row_begin + local) return g - row_begin + halo_lo;
+        if (g >= lo_src && g < lo_src + halo_lo) return g - lo_src;
+        if (g >= hi_src && g < hi_src + halo_hi) return g - hi_src + halo_lo + local;
+        return -2;
+    }
+};
+inline ColMap colmap_of(const Partition& p) {
+    return ColMap{p.row_begin, p.local, p.halo_lo, p.halo_hi, p.lo_src_begin, p.hi_src_begin};
+}
+
 struct Context;
 
 // ---- SELL-C-sigma matrix (C = 32, sigma = 1) ---------------------------------------
@@ -226,7 +246,15 @@ void host_randomize(int kind, uint64_t seed, int64_t first, int64_t count, void*
 std::vector<double> window_coeffs(double tlo, double thi, double blo, double bhi, int degree);
 std::vector<double> kernel_coeffs(int kind, int mu, int degree);
 double dos_count(const double* mu, int order, double blo, double bhi, double lo, double hi);
+struct HostCsr;
+// Halos of rows [r0, r1) derived from the global columns they read (ring
+// distance decides lower vs upper neighbour); starts[q] = first row of rank q.
+Partition plan_rows(const HostCsr& csr, int64_t r0, int64_t r1, const std::vector<int64_t>& starts);
+// Send ranges from every rank's (halo_lo, halo_hi, lo_rank, hi_rank) (all4).
+void plan_sends(Partition& p, int rank, int nranks, const int64_t* all4);
 // plane partition of `dim` rows into nranks parts, boundaries on multiples of `plane`
 void plane_partition(int64_t dim, int64_t plane, int rank, int nranks, int64_t* r0, int64_t* r1);
+// first row of every rank for the lattice models (TI z-planes, graphene y-rows)
+void lattice_starts(const chebfd_lattice& s, bool ti, int nranks, std::vector<int64_t>& starts);
 
 }  // namespace cfd

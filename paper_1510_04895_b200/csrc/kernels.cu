@@ -709,16 +709,6 @@ __global__ void sell_width_kernel(const int64_t* __restrict__ offs, int64_t rows
     atomicMax(maxlen, static_cast<int>(w));
 }
 
-struct ColMap {
-    int64_t row_begin, local, halo_lo, halo_hi, lo_src, hi_src;
-    __device__ int map(int64_t g) const {
-        if (g >= row_begin && g < row_begin + local) return static_cast<int>(g - row_begin + halo_lo);
-        if (g >= lo_src && g < lo_src + halo_lo) return static_cast<int>(g - lo_src);
-        if (g >= hi_src && g < hi_src + halo_hi) return static_cast<int>(g - hi_src + halo_lo + local);
-        return -2;  // not representable: error
-    }
-};
-
 template <class M>
 __global__ void sell_fill_kernel(const int64_t* __restrict__ offs, const int64_t* __restrict__ gcols,
                                  const M* __restrict__ gvals, int64_t rows,
@@ -735,7 +725,7 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ offs, const int64_t
     for (int64_t j = 0; j < width; ++j) {
         const int64_t slot = base + j * kChunk + lane;
         if (b + j < e) {
-            const int c = cm.map(gcols[b + j]);
+            const int c = static_cast<int>(cm.map(gcols[b + j]));
             if (c < 0) atomicExch(err, 1);
             cols[slot] = c;
             vals[slot] = gvals[b + j];
@@ -1076,8 +1066,7 @@ void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d
         fail(CHEBFD_ERR_UNSUPPORTED, "extended row count exceeds int32 column indices");
     m.cols.ensure(sizeof(int) * std::max<int64_t>(entries, 1));
     m.vals.ensure((m.kind ? 16 : 8) * std::max<int64_t>(entries, 1));
-    ColMap cm{m.part.row_begin, m.part.local, m.part.halo_lo, m.part.halo_hi, m.part.lo_src_begin,
-              m.part.hi_src_begin};
+    const ColMap cm = colmap_of(m.part);
     const int64_t threads = m.nchunks * kChunk;
     if (threads > 0) {
         const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
