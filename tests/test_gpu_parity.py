@@ -219,3 +219,18 @@ def test_gram_kahan_exact_count(ctx):
     A = cf.SparseMatrix.from_csr(ctx, n, np.arange(n + 1), np.arange(n), np.ones(n))
     X = cf.BlockVector(A, 1).upload(np.ones((n, 1)))
     assert cf.gram(X, X)[0, 0] == 1000.0
+
+
+def test_cpp_dropin_layer_on_device(lib_built, tmp_path):
+    """include/chebfd_b200.hpp used from C++ against the device (tests/cpp)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "use"
+    r = subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", f"-I{root}/include",
+                        os.path.join(root, "tests", "cpp", "use_wrapper.cpp"), "-o", str(out),
+                        f"-L{os.path.dirname(lib_built)}", "-lchebfd_b200",
+                        f"-Wl,-rpath,{os.path.dirname(lib_built)}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    run = subprocess.run([str(out)], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stdout + run.stderr
