@@ -316,7 +316,10 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
     const int64_t r0 = starts[c.rank], r1 = starts[c.rank + 1];
     HostCsr csr = ti ? gen_topological_insulator(s, r0, r1) : gen_graphene(s, r0, r1);
     const int64_t nnz_g = allreduce_count(c, static_cast<int64_t>(csr.cols.size()));
-    return matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g);
+    auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g);
+    m->plane_rows = ti ? 4 * s.lx * s.ly : 2 * s.lx;
+    m->line_rows = ti ? 4 * s.lx : 0;
+    return m;
 }
 
 // --------------------------------------------------------- apply_filter --
@@ -496,6 +499,9 @@ static void ctx_init(Context& c, int device) {
     c.device = device;
     CFD_CUDA(cudaSetDevice(device));
     CFD_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+    int l2 = 0;
+    CFD_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+    if (l2 > 0) c.l2_bytes = l2;
     CFD_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     CFD_CUDA(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking));
     CFD_CUDA(cudaEventCreateWithFlags(&c.ev_a, cudaEventDisableTiming));
@@ -578,6 +584,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->overlap = value != 0;
         else if (option == CHEBFD_OPT_KERNEL)
             c->kernel_variant = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PLANE_ORDER)
+            c->plane_order = static_cast<int>(value);
         else
             fail(CHEBFD_ERR_INVALID_ARGUMENT, "unknown option");
     });

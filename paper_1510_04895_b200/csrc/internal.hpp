@@ -94,6 +94,8 @@ struct Matrix {
     int kind = 0;
     int64_t nnz_global = 0, nnz_local = 0;
     int max_row_len = 0;
+    int64_t plane_rows = 0;  // lattice plane (TI z-plane, graphene y-row); 0 = unknown
+    int64_t line_rows = 0;   // one lattice line inside a plane (TI y-row of sites)
     Partition part;
     int64_t nchunks = 0;
     int64_t entries = 0;     // SELL slots (padding included)
@@ -154,6 +156,8 @@ struct FilterWorkspace {
 
 struct Context {
     int device = 0, rank = 0, nranks = 1, num_sms = 148;
+    double l2_bytes = 126.0 * (1 << 20);
+    int plane_order = 0;  // tile order: 0 natural; Y > 0: 2.5D bands of Y lines swept through all planes
     cudaStream_t stream = nullptr;       // compute
     cudaStream_t comm_stream = nullptr;  // halo exchange
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;

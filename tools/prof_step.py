@@ -21,12 +21,16 @@ def main():
     ap.add_argument("--nb", type=int, default=32)
     ap.add_argument("--model", default="ti", choices=["ti", "graphene"])
     ap.add_argument("--moments", action="store_true")
+    ap.add_argument("--lz", type=int, default=0, help="TI z extent (default = lattice)")
+    ap.add_argument("--plane-order", type=int, default=0)
     args = ap.parse_args()
     ctx = cf.Context(0)
     ctx.set_option("kernel", args.kernel)
+    ctx.set_option("plane_order", args.plane_order)
     L = args.lattice
     if args.model == "ti":
-        A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(L, L, L, disorder=0.5))
+        A = cf.SparseMatrix.topological_insulator(
+            ctx, cf.LatticeSpec(L, L, args.lz or L, disorder=0.5))
         s_d = 16
     else:
         A = cf.SparseMatrix.graphene(ctx, cf.LatticeSpec(L, L, disorder=1.0))
