@@ -252,6 +252,35 @@ int chebfd_kpm_dos(chebfd_matrix* a, double bounds_lo, double bounds_hi, int ord
 int chebfd_dos_count(const double* mu, int order, double bounds_lo, double bounds_hi, double lo,
                      double hi, double* out);
 
+/* ---- filter design (filter_design.hpp / filter_design.cpp) ------------------------ */
+typedef struct {
+    int np_opt;              /* optimal degree N_p */
+    double eta_opt;          /* spMVMs per vector per decade of damping */
+    double sigma;            /* damping factor of the optimal filter */
+    double predicted_mvms;   /* eta_opt * (-log10 eps) */
+    int predicted_iters;     /* ceil(log10 eps / log10 sigma) */
+    double delta_prime;      /* search margin used */
+    double n_target_estimate;
+    int below_recommended_search_space; /* N_S < 1.25 N_T */
+} chebfd_design;
+/* damping_factor (filter_design.cpp:178-184) for the window on [tlo,thi] with
+ * search margin delta' inside [blo,bhi] */
+int chebfd_damping_factor(double target_lo, double target_hi, double delta_prime,
+                          double bounds_lo, double bounds_hi, int degree, int kernel, int mu,
+                          double* sigma);
+/* optimize_degree (filter_design.cpp:204-277) */
+int chebfd_optimize_degree(double target_lo, double target_hi, double delta_prime,
+                           double bounds_lo, double bounds_hi, int kernel, int mu, double epsilon,
+                           chebfd_design* out);
+/* invert_search_margin (filter_design.cpp:330-354) from raw KPM moments */
+int chebfd_invert_search_margin(const double* mu, int order, double bounds_lo, double bounds_hi,
+                                double target_lo, double target_hi, double n_search,
+                                double* delta_prime);
+/* choose_parameters (filter_design.cpp:356-369) from raw KPM moments */
+int chebfd_choose_parameters(const double* mu, int order, double bounds_lo, double bounds_hi,
+                             double target_lo, double target_hi, double n_search, int kernel,
+                             int kernel_mu, double epsilon, chebfd_design* out);
+
 /* ---- full ChebFD driver (solver.cpp:93-214) ------------------------------------- */
 typedef struct {
     double target_lo, target_hi;

@@ -13,7 +13,8 @@ from .api import (  # noqa: F401
     kernel_coeffs, kpm_dos, lanczos_bounds, make_filter, per_row_bytes, per_row_flops,
     plan_all4, plan_complete_sends, plan_map_column, plan_partition, plan_sends,
     rayleigh_ritz, recurrence_step, solve, spmmvm, spmmvm_fused, svqb_orthonormalize,
-    window_coeffs,
+    window_coeffs, DesignResult, choose_parameters, damping_factor, invert_search_margin,
+    optimize_degree, quality,
 )
 from ._lib import LIB_PATH, load  # noqa: F401
 

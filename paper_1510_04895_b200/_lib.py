@@ -39,6 +39,12 @@ class chebfd_matrix_info(C.Structure):
                 ("halo_lo", _i64), ("halo_hi", _i64), ("chunk", _int), ("max_row_len", _int)]
 
 
+class chebfd_design(C.Structure):
+    _fields_ = [("np_opt", _int), ("eta_opt", _dbl), ("sigma", _dbl), ("predicted_mvms", _dbl),
+                ("predicted_iters", _int), ("delta_prime", _dbl), ("n_target_estimate", _dbl),
+                ("below_recommended_search_space", _int)]
+
+
 class chebfd_solver_options(C.Structure):
     _fields_ = [("target_lo", _dbl), ("target_hi", _dbl), ("epsilon", _dbl), ("n_search", _int),
                 ("degree", _int), ("kernel", _int), ("kernel_mu", _int), ("max_iters", _int),
@@ -111,6 +117,11 @@ _SIGS = {
     "chebfd_lanczos_bounds": (_int, [_vp, _int, _u64, _vp, _vp]),
     "chebfd_kpm_dos": (_int, [_vp, _dbl, _dbl, _int, _int, _u64, _vp]),
     "chebfd_dos_count": (_int, [_vp, _int, _dbl, _dbl, _dbl, _dbl, _vp]),
+    "chebfd_damping_factor": (_int, [_dbl, _dbl, _dbl, _dbl, _dbl, _int, _int, _int, _vp]),
+    "chebfd_optimize_degree": (_int, [_dbl, _dbl, _dbl, _dbl, _dbl, _int, _int, _dbl, _vp]),
+    "chebfd_invert_search_margin": (_int, [_vp, _int, _dbl, _dbl, _dbl, _dbl, _dbl, _vp]),
+    "chebfd_choose_parameters": (_int, [_vp, _int, _dbl, _dbl, _dbl, _dbl, _dbl, _int, _int, _dbl,
+                                        _vp]),
     "chebfd_solver_options_default": (None, [_vp]),
     "chebfd_solve": (_int, [_vp, _vp, _vp, _int, _vp, _vp, _vp, _vp, _pp]),
 }

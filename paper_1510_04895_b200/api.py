@@ -775,3 +775,72 @@ def plan_complete_sends(plans) -> None:
 def plan_map_column(plan, g: int) -> int:
     """Extended-row index of global column g on this rank (-2: not held)."""
     return int(_lib().chebfd_plan_map_column(C.byref(plan), int(g)))
+
+
+# --------------------------------------------------------- filter design --
+@dataclass
+class DesignResult:
+    """filter_design.hpp:21-28 (+ the margin and N_T used)."""
+    np_opt: int
+    eta_opt: float
+    sigma: float
+    predicted_mvms: float
+    predicted_iters: int
+    delta_prime: float
+    n_target_estimate: float = 0.0
+    below_recommended_search_space: bool = False
+
+
+def _design(d):
+    return DesignResult(d.np_opt, d.eta_opt, d.sigma, d.predicted_mvms, d.predicted_iters,
+                        d.delta_prime, d.n_target_estimate, bool(d.below_recommended_search_space))
+
+
+def damping_factor(p: FilterPolynomial, delta_prime: float) -> float:
+    """sigma of filter p for the search margin delta' (filter_design.cpp:178-184)."""
+    k, mu = p.kernel.code()
+    s = C.c_double()
+    _check(_lib().chebfd_damping_factor(p.target.lo, p.target.hi, delta_prime, p.bounds.lo,
+                                        p.bounds.hi, p.degree, k, mu, C.byref(s)))
+    return s.value
+
+
+def optimize_degree(target, delta_prime, bounds, kernel="lanczos2", epsilon=1e-12) -> DesignResult:
+    """filter_design.cpp:204-277"""
+    t, b = _iv(target), _iv(bounds)
+    k, mu = _kernel(kernel).code()
+    d = L.chebfd_design()
+    _check(_lib().chebfd_optimize_degree(t.lo, t.hi, delta_prime, b.lo, b.hi, k, mu, epsilon,
+                                         C.byref(d)))
+    return _design(d)
+
+
+def invert_search_margin(dos: DosEstimate, target, n_search: float) -> float:
+    """filter_design.cpp:330-354"""
+    t = _iv(target)
+    mu = np.ascontiguousarray(dos.moments, dtype=np.float64)
+    out = C.c_double()
+    _check(_lib().chebfd_invert_search_margin(_ptr(mu), len(mu) - 1, dos.bounds.lo, dos.bounds.hi,
+                                              t.lo, t.hi, n_search, C.byref(out)))
+    return out.value
+
+
+def choose_parameters(dos: DosEstimate, target, n_search: float, kernel="lanczos2",
+                      epsilon=1e-12) -> DesignResult:
+    """filter_design.cpp:356-369"""
+    t = _iv(target)
+    k, kmu = _kernel(kernel).code()
+    mu = np.ascontiguousarray(dos.moments, dtype=np.float64)
+    d = L.chebfd_design()
+    _check(_lib().chebfd_choose_parameters(_ptr(mu), len(mu) - 1, dos.bounds.lo, dos.bounds.hi,
+                                           t.lo, t.hi, n_search, k, kmu, epsilon, C.byref(d)))
+    return _design(d)
+
+
+def quality(degree: int, sigma: float) -> float:
+    """filter_design.cpp:186-190"""
+    if not sigma > 0.0:
+        raise DomainError("quality: sigma must be positive")
+    if sigma >= 1.0:
+        raise DomainError("quality: sigma >= 1, filter does not damp")
+    return -degree / np.log10(sigma)

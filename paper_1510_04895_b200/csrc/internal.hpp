@@ -256,6 +256,21 @@ struct HostCsr;
 Partition plan_rows(const HostCsr& csr, int64_t r0, int64_t r1, const std::vector<int64_t>& starts);
 // Send ranges from every rank's (halo_lo, halo_hi, lo_rank, hi_rank) (all4).
 void plan_sends(Partition& p, int rank, int nranks, const int64_t* all4);
+// filter design (design.cpp, restating filter_design.cpp)
+struct DesignOut {
+    int np_opt = 0, predicted_iters = 0;
+    double eta_opt = 0, sigma = 0, predicted_mvms = 0, delta_prime = 0, n_target_estimate = 0;
+    bool below_recommended = false;
+};
+double quality_of(int degree, double sigma);
+double damping_factor(double tlo, double thi, double dprime, double blo, double bhi, int degree,
+                      int kind, int mu);
+DesignOut optimize_degree(double tlo, double thi, double dprime, double blo, double bhi, int kind,
+                          int mu, double epsilon);
+double invert_search_margin(const double* mu, int order, double blo, double bhi, double tlo,
+                            double thi, double n_search);
+DesignOut choose_parameters(const double* mu, int order, double blo, double bhi, double tlo,
+                            double thi, double n_search, int kind, int kmu, double epsilon);
 // plane partition of `dim` rows into nranks parts, boundaries on multiples of `plane`
 void plane_partition(int64_t dim, int64_t plane, int rank, int nranks, int64_t* r0, int64_t* r1);
 // first row of every rank for the lattice models (TI z-planes, graphene y-rows)

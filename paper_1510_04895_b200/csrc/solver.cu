@@ -406,11 +406,24 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
                                         : 2 * static_cast<int>(std::ceil(rep->n_target_estimate));
         if (o->degree > 0) {
             rep->degree = o->degree;
-            rep->sigma = 0.0;  // filter-design report of an imposed degree: not computed
-            rep->eta = 0.0;
-        } else {
-            fail(CHEBFD_ERR_UNSUPPORTED,
-                 "solve: automatic degree selection (choose_parameters) not available; pass degree");
+            // sigma / eta of the imposed degree, for reporting only (solver.cpp:114-129)
+            try {
+                const double dp = invert_search_margin(mu.data(), o->dos_moments, blo, bhi,
+                                                       o->target_lo, o->target_hi, rep->n_search);
+                rep->sigma = damping_factor(o->target_lo, o->target_hi, dp, blo, bhi, rep->degree,
+                                            o->kernel, o->kernel_mu);
+                rep->eta = rep->sigma < 1.0 ? quality_of(rep->degree, rep->sigma) : 0.0;
+            } catch (const std::exception&) {
+                rep->sigma = 0.0;
+                rep->eta = 0.0;
+            }
+        } else {  // choose_parameters (solver.cpp:130-136)
+            const DesignOut d = choose_parameters(mu.data(), o->dos_moments, blo, bhi, o->target_lo,
+                                                  o->target_hi, rep->n_search, o->kernel,
+                                                  o->kernel_mu, o->epsilon);
+            rep->degree = d.np_opt;
+            rep->sigma = d.sigma;
+            rep->eta = d.eta_opt;
         }
         if (rep->degree < 2) fail(CHEBFD_ERR_RUNTIME, "solve: filter degree must be >= 2");
         const int np = rep->degree;
