@@ -23,6 +23,10 @@
 #include <cub/device/device_scan.cuh>
 #include <type_traits>
 
+#ifndef CFD_TMA_MINB
+#define CFD_TMA_MINB 2  // resident CTAs per SM the TMA step kernel is compiled for
+#endif
+
 #include "internal.hpp"
 
 namespace cfd {
@@ -429,7 +433,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 }
 
 template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
-__global__ void __launch_bounds__(256, 2) step_tma_kernel(const StepParams p) {
+__global__ void __launch_bounds__(256, CFD_TMA_MINB) step_tma_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
     constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
