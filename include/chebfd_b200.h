@@ -302,6 +302,9 @@ typedef struct {
     int converged, iterations, n_search, degree, n_values;
     double total_spmvms, sigma, eta, bounds_lo, bounds_hi, matrix_norm_est, n_target_estimate;
     double seconds, weight_integral;
+    /* wall seconds per phase: Lanczos bounds, KPM DOS, filter design, all
+     * apply_filter calls, SVQB (incl. rank repair), Rayleigh-Ritz */
+    double t_bounds, t_dos, t_design, t_filter, t_ortho, t_rr;
 } chebfd_solve_report;
 
 /* values/residual_norms/accepted: capacity `cap` >= n_search; history:

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libchebfd_b200.so")
+# CHEBFD_B200_LIB overrides the library path (A/B builds); default: the in-tree build
+LIB_PATH = os.environ.get("CHEBFD_B200_LIB", os.path.join(HERE, "libchebfd_b200.so"))
 
 _i64 = C.c_int64
 _u64 = C.c_uint64
@@ -56,7 +57,9 @@ class chebfd_solve_report(C.Structure):
     _fields_ = [("converged", _int), ("iterations", _int), ("n_search", _int), ("degree", _int),
                 ("n_values", _int), ("total_spmvms", _dbl), ("sigma", _dbl), ("eta", _dbl),
                 ("bounds_lo", _dbl), ("bounds_hi", _dbl), ("matrix_norm_est", _dbl),
-                ("n_target_estimate", _dbl), ("seconds", _dbl), ("weight_integral", _dbl)]
+                ("n_target_estimate", _dbl), ("seconds", _dbl), ("weight_integral", _dbl),
+                ("t_bounds", _dbl), ("t_dos", _dbl), ("t_design", _dbl), ("t_filter", _dbl),
+                ("t_ortho", _dbl), ("t_rr", _dbl)]
 
 
 _SIGS = {

@@ -683,6 +683,7 @@ class ConvergenceReport:
     weight_integral: float
     have_weight: bool
     seconds: float
+    timings: dict = field(default_factory=dict)  # wall seconds per solve phase
 
 
 def solve(A: SparseMatrix, opts: SolverOptions) -> ConvergenceReport:
@@ -720,7 +721,9 @@ def solve(A: SparseMatrix, opts: SolverOptions) -> ConvergenceReport:
                              rep.degree, rep.sigma, rep.eta, Interval(rep.bounds_lo, rep.bounds_hi),
                              rep.matrix_norm_est, rep.n_target_estimate, ritz,
                              hist[:rep.iterations].copy(), rep.weight_integral,
-                             bool(opts.collect_weight_density), rep.seconds)
+                             bool(opts.collect_weight_density), rep.seconds,
+                             {k: getattr(rep, "t_" + k) for k in
+                              ("bounds", "dos", "design", "filter", "ortho", "rr")})
 
 
 # ----------------------------------------------------- bench conventions --

@@ -800,7 +800,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     const int64_t nrows = s.row1 - s.row0;
     constexpr int MW = MAXW > 0 ? MAXW : 4;
     const void* svals = s.alpha == 1.0 ? a.vals.p : find_scaled(a, s.alpha);
-    const bool tma = MAXW > 0 && ctx.kernel_variant == 1 && svals != nullptr;
+    const bool tma = MAXW > 0 && ctx.kernel_variant >= 1 && svals != nullptr;
     auto kernel = tma ? step_tma_kernel<CPLX, T, KIND, DMODE, MW>
                       : step_kernel<CPLX, T, KIND, DMODE, 0>;
     int used_total = 0;
@@ -810,9 +810,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         Geometry g = tma ? geometry_pow2(us) : geometry(us);
         const int TR = std::max(32, g.R);
         const size_t stage = tma ? 2 * static_cast<size_t>(MW) * TR : 0;
-        const size_t ring = tma ? ((stage * sizeof(int) + 15) & ~size_t(15)) +
-                                      stage * (CPLX ? 16 : 8)
-                                : 0;
+        size_t ring = tma ? ((stage * sizeof(int) + 15) & ~size_t(15)) + stage * (CPLX ? 16 : 8)
+                          : 0;
         const size_t smem = std::max(NDOT * static_cast<size_t>(g.threads) * sizeof(T), ring);
         if (smem > 48 * 1024) {
             static thread_local std::map<const void*, size_t> attr_set;

@@ -385,12 +385,21 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
         if (!(o->target_lo < o->target_hi))
             fail(CHEBFD_ERR_INVALID_ARGUMENT, "solve: degenerate target");
         std::memset(rep, 0, sizeof(*rep));
+        using clk = std::chrono::steady_clock;
+        auto secs = [](clk::time_point a) {
+            return std::chrono::duration<double>(clk::now() - a).count();
+        };
+        auto tp = clk::now();
         double blo = o->bounds_lo, bhi = o->bounds_hi;
         if (!(blo < bhi)) lanczos_bounds(c, A, 30, o->seed, &blo, &bhi);
+        rep->t_bounds = secs(tp);
+        tp = clk::now();
         rep->bounds_lo = blo;
         rep->bounds_hi = bhi;
         rep->matrix_norm_est = std::max(std::abs(blo), std::abs(bhi));
         const auto mu = kpm_dos(c, A, blo, bhi, o->dos_moments, o->dos_samples, o->seed + 1);
+        rep->t_dos = secs(tp);
+        tp = clk::now();
         // estimate_count (spectral.cpp:90-94)
         if (!(blo <= o->target_lo && o->target_hi <= bhi))
             fail(CHEBFD_ERR_INVALID_ARGUMENT, "estimate_count: interval outside DOS bounds");
@@ -425,6 +434,7 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
             rep->sigma = d.sigma;
             rep->eta = d.eta_opt;
         }
+        rep->t_design = secs(tp);
         if (rep->degree < 2) fail(CHEBFD_ERR_RUNTIME, "solve: filter degree must be >= 2");
         const int np = rep->degree;
         std::vector<double> combined(np + 1);
@@ -447,8 +457,12 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
         std::vector<double> mom;
         for (int iter = 1; iter <= o->max_iters; ++iter) {
             if (o->collect_weight_density) mom.assign(static_cast<size_t>(np + 1) * x->width, 0.0);
+            tp = clk::now();
             apply_filter_device(c, A, *x, combined.data(), np, alpha, beta,
                                 o->collect_weight_density ? mom.data() : nullptr);
+            ctx_sync(c);
+            rep->t_filter += secs(tp);
+            tp = clk::now();
             if (o->collect_weight_density) {
                 double w0 = 0.0;  // weight_density mu[0] = sum_k m(0,k) (spectral.cpp:81-88)
                 for (int64_t k = 0; k < x->width; ++k) w0 += mom[k];
@@ -463,7 +477,10 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
                 launch_copy_columns(c, *padded, ortho.rank, *fresh, 0, ns - ortho.rank, c.stream);
                 ortho = svqb(c, &A, *padded, 1e-14);
             }
+            rep->t_ortho += secs(tp);
+            tp = clk::now();
             ritz = rayleigh_ritz(c, A, *ortho.q);
+            rep->t_rr += secs(tp);
             const int64_t nb = ritz.vectors->width;
             int acc = 0, pending = 0;
             double rmin = 0.0, rmax = 0.0;

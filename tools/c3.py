@@ -62,6 +62,7 @@ def main():
             "accepted_in_window": bool(np.all(np.abs(vals) <= h)),
             "total_spmvms": rep.total_spmvms, "solve_s": round(dt, 2),
             "matrix_build_s": round(t_build, 2),
+            "timings_s": {k: round(v, 3) for k, v in rep.timings.items()},
             "history": rep.history.tolist()}), flush=True)
     ctx.close()
 
