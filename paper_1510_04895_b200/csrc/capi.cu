@@ -97,7 +97,7 @@ void purge_graphs(Context& c, const void* a, const void* x) {
 }
 
 std::unique_ptr<Block> make_block(Context& c, const Matrix* m, int kind, int64_t rows,
-                                  int64_t width) {
+                                  int64_t width, bool zero) {
     require(width >= 0 && rows >= 0, "BlockVector: negative shape");
     auto b = std::make_unique<Block>();
     b->ctx = &c;
@@ -116,7 +116,15 @@ std::unique_ptr<Block> make_block(Context& c, const Matrix* m, int kind, int64_t
     const size_t bytes = static_cast<size_t>((b->halo_lo + rows + b->halo_hi) * width) *
                          b->scalar_bytes();
     b->buf.ensure(std::max<size_t>(bytes, 256));
-    CFD_CUDA(cudaMemsetAsync(b->buf.p, 0, b->buf.bytes, c.stream));
+    if (zero) {
+        CFD_CUDA(cudaMemsetAsync(b->buf.p, 0, b->buf.bytes, c.stream));
+    } else {
+        const size_t rb = static_cast<size_t>(width) * b->scalar_bytes();
+        if (b->halo_lo) CFD_CUDA(cudaMemsetAsync(b->buf.p, 0, b->halo_lo * rb, c.stream));
+        if (b->halo_hi)
+            CFD_CUDA(cudaMemsetAsync(static_cast<char*>(b->owned()) + rows * rb, 0, b->halo_hi * rb,
+                                     c.stream));
+    }
     return b;
 }
 
@@ -326,9 +334,9 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
 FilterWorkspace& filter_workspace(Context& c, const Matrix& a, int64_t width, bool moments) {
     auto key = std::make_tuple(static_cast<const void*>(&a), width, a.kind);
     FilterWorkspace& ws = c.filter_ws[key];
-    if (!ws.u) ws.u = make_block(c, &a, a.kind, a.part.local, width);
-    if (!ws.w) ws.w = make_block(c, &a, a.kind, a.part.local, width);
-    if (moments && !ws.x0) ws.x0 = make_block(c, &a, a.kind, a.part.local, width);
+    if (!ws.u) ws.u = make_block(c, &a, a.kind, a.part.local, width, false);
+    if (!ws.w) ws.w = make_block(c, &a, a.kind, a.part.local, width, false);
+    if (moments && !ws.x0) ws.x0 = make_block(c, &a, a.kind, a.part.local, width, false);
     return ws;
 }
 

@@ -30,8 +30,10 @@ int guard(F&& f) {
 void cublas_check(int st, const char* what);
 void nccl_check(int st, const char* what);
 void ctx_sync(Context& c);
+// zero = false: only the halo rows are cleared (for blocks every owned row of
+// which the caller overwrites before reading)
 std::unique_ptr<Block> make_block(Context& c, const Matrix* m, int kind, int64_t rows,
-                                  int64_t width);
+                                  int64_t width, bool zero = true);
 void check_same_shape(const Block& x, const Block& y);
 void check_conforms(const Matrix& a, const Block& x, const char* who);
 void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered);

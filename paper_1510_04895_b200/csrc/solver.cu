@@ -82,7 +82,7 @@ SvqbOut svqb(Context& c, const Matrix* shape, Block& y, double drop_tol) {
         }
     }
     SvqbOut out;
-    out.q = make_block(c, shape, y.kind, y.rows, r);
+    out.q = make_block(c, shape, y.kind, y.rows, r, false);
     mult_small_host_b(c, y, cm.a.data(), r, *out.q);
     out.rank = r;
     return out;
@@ -96,7 +96,7 @@ struct Ritz {
 // rayleigh_ritz (solver.cpp:63-91)
 Ritz rayleigh_ritz(Context& c, const Matrix& a, Block& q) {
     const int64_t nb = q.width;
-    auto aq = make_block(c, &a, q.kind, q.rows, nb);
+    auto aq = make_block(c, &a, q.kind, q.rows, nb, false);
     StepArgs s{};
     s.kind_step = kStepSpmmvm;
     s.w = aq->owned();
@@ -111,8 +111,8 @@ Ritz rayleigh_ritz(Context& c, const Matrix& a, Block& q) {
     Small rot(q.kind, nb, nb);
     if (!heev_host(c, q.kind, nb, p.a.data(), out.values.data(), rot.a.data(), true))
         fail(CHEBFD_ERR_RUNTIME, "rayleigh_ritz: projected eigensolve failed");
-    out.vectors = make_block(c, &a, q.kind, q.rows, nb);
-    auto av = make_block(c, &a, q.kind, q.rows, nb);
+    out.vectors = make_block(c, &a, q.kind, q.rows, nb, false);
+    auto av = make_block(c, &a, q.kind, q.rows, nb, false);
     DeviceBuffer drot(std::max<size_t>(rot.a.size() * sizeof(double), 16));
     CFD_CUDA(cudaMemcpyAsync(drot.p, rot.a.data(), rot.a.size() * sizeof(double),
                              cudaMemcpyHostToDevice, c.stream));
@@ -181,7 +181,7 @@ void lanczos_bounds(Context& c, const Matrix& a, int iters, uint64_t seed, doubl
     const int64_t d = a.part.dim;
     const int m = static_cast<int>(std::min<int64_t>(iters, d));
     for (int restart = 0; restart < 4; ++restart) {
-        auto v = make_block(c, &a, a.kind, a.part.local, 1);
+        auto v = make_block(c, &a, a.kind, a.part.local, 1, false);
         randomize(c, *v, seed + 977 * restart);
         divide_columns(c, *v, norms(c, *v));
         std::vector<std::unique_ptr<Block>> basis;
@@ -190,7 +190,7 @@ void lanczos_bounds(Context& c, const Matrix& a, int iters, uint64_t seed, doubl
         for (int j = 0; j < m; ++j) {
             basis.push_back(std::move(v));
             Block& last = *basis.back();
-            auto w = make_block(c, &a, a.kind, a.part.local, 1);
+            auto w = make_block(c, &a, a.kind, a.part.local, 1, false);
             StepArgs s{};
             s.kind_step = kStepSpmmvm;
             s.w = w->owned();
@@ -236,11 +236,11 @@ std::vector<double> kpm_dos(Context& c, const Matrix& a, double blo, double bhi,
     const int64_t d = a.part.dim;
     const double alpha = 2.0 / (bhi - blo);
     const double beta = (blo + bhi) / (blo - bhi);
-    auto z = make_block(c, &a, a.kind, a.part.local, samples);
+    auto z = make_block(c, &a, a.kind, a.part.local, samples, false);
     randomize(c, *z, seed);
     divide_columns(c, *z, norms(c, *z));
-    auto u = make_block(c, &a, a.kind, a.part.local, samples);
-    auto w = make_block(c, &a, a.kind, a.part.local, samples);
+    auto u = make_block(c, &a, a.kind, a.part.local, samples, false);
+    auto w = make_block(c, &a, a.kind, a.part.local, samples, false);
     const int nchecks = order / 128;
     DeviceBuffer mom(sizeof(double) * (order + 1) * samples);
     const size_t nrm_row = static_cast<size_t>(samples) * (a.kind ? 2 : 1);
@@ -450,7 +450,7 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
         const double required =
             std::max(1.0, std::ceil(rep->n_target_estimate - 3.0 * std::sqrt(rep->n_target_estimate)));
         const int64_t ns = rep->n_search;
-        auto x = make_block(c, &A, A.kind, A.part.local, ns);
+        auto x = make_block(c, &A, A.kind, A.part.local, ns, false);
         randomize(c, *x, o->seed + 2);
         divide_columns(c, *x, norms(c, *x));  // unit columns (solver.cpp:149-154)
         Ritz ritz;
@@ -470,8 +470,8 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
             }
             SvqbOut ortho = svqb(c, &A, *x, 1e-14);
             for (int repair = 0; ortho.rank < ns && repair < 5; ++repair) {
-                auto padded = make_block(c, &A, A.kind, A.part.local, ns);
-                auto fresh = make_block(c, &A, A.kind, A.part.local, ns - ortho.rank);
+                auto padded = make_block(c, &A, A.kind, A.part.local, ns, false);
+                auto fresh = make_block(c, &A, A.kind, A.part.local, ns - ortho.rank, false);
                 randomize(c, *fresh, o->seed + 1000 + iter * 13 + repair);
                 launch_copy_columns(c, *padded, 0, *ortho.q, 0, ortho.rank, c.stream);
                 launch_copy_columns(c, *padded, ortho.rank, *fresh, 0, ns - ortho.rank, c.stream);
