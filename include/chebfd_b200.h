@@ -183,6 +183,10 @@ int chebfd_block_zero(chebfd_block* b);
  * libstdc++ normal_distribution stream over the GLOBAL D x nb block, so a
  * distributed block equals the reference's rows. Host-generated, uploaded. */
 int chebfd_block_randomize(chebfd_block* b, uint64_t seed);
+/* Host: entries [first, first+count) of that stream for a global block of
+ * kind `kind` (row-major; complex entries interleaved), generated in parallel
+ * with mt19937_64 jump-ahead, bit-identical to the reference. */
+int chebfd_host_randomize(int kind, uint64_t seed, int64_t first, int64_t count, void* out);
 /* Device Gaussian fill (Philox counter RNG) -- fast synthetic inputs for
  * benchmarks; NOT the reference's stream. */
 int chebfd_block_randomize_device(chebfd_block* b, uint64_t seed);

@@ -14,7 +14,7 @@ from .api import (  # noqa: F401
     plan_all4, plan_complete_sends, plan_map_column, plan_partition, plan_sends,
     rayleigh_ritz, recurrence_step, solve, spmmvm, spmmvm_fused, svqb_orthonormalize,
     window_coeffs, DesignResult, choose_parameters, damping_factor, invert_search_margin,
-    optimize_degree, quality,
+    optimize_degree, quality, host_randomize,
 )
 from ._lib import LIB_PATH, load  # noqa: F401
 

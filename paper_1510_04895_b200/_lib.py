@@ -98,6 +98,7 @@ _SIGS = {
     "chebfd_block_zero": (_int, [_vp]),
     "chebfd_block_randomize": (_int, [_vp, _u64]),
     "chebfd_block_randomize_device": (_int, [_vp, _u64]),
+    "chebfd_host_randomize": (_int, [_int, _u64, _i64, _i64, _vp]),
     "chebfd_block_scale_columns": (_int, [_vp, _vp]),
     "chebfd_block_copy_columns": (_int, [_vp, _i64, _vp, _i64, _i64]),
     "chebfd_block_device_ptr": (_int, [_vp, _pp]),

@@ -847,3 +847,15 @@ def quality(degree: int, sigma: float) -> float:
     if sigma >= 1.0:
         raise DomainError("quality: sigma >= 1, filter does not damp")
     return -degree / np.log10(sigma)
+
+
+def host_randomize(dim: int, width: int, seed: int, complex_: bool = False, first_row: int = 0,
+                   rows=None) -> np.ndarray:
+    """Rows [first_row, first_row+rows) of BlockVector(dim, width).randomize(seed)
+    (block_vector.hpp:42-51) -- the reference's exact stream, generated on the
+    host in parallel (mt19937_64 jump-ahead)."""
+    rows = dim - first_row if rows is None else rows
+    out = np.empty((rows, width), dtype=np.complex128 if complex_ else np.float64)
+    _check(_lib().chebfd_host_randomize(int(complex_), seed, first_row * width, rows * width,
+                                        _ptr(out)))
+    return out

@@ -208,29 +208,6 @@ HostCsr gen_topological_insulator(const chebfd_lattice& s, int64_t r0, int64_t r
     return out;
 }
 
-// BlockVector::randomize (block_vector.hpp:42-51): std::mt19937_64 feeding
-// std::normal_distribution<double>; complex entries are
-// Complex(dist(gen), dist(gen)) whose arguments GCC evaluates right to left
-// (imaginary part drawn first).  Entries [first, first+count) of the stream.
-void host_randomize(int kind, uint64_t seed, int64_t first, int64_t count, void* out) {
-    std::mt19937_64 gen(seed);
-    std::normal_distribution<double> dist(0.0, 1.0);
-    if (kind == CHEBFD_REAL64) {
-        for (int64_t i = 0; i < first; ++i) (void)dist(gen);
-        double* o = static_cast<double*>(out);
-        for (int64_t i = 0; i < count; ++i) o[i] = dist(gen);
-    } else {
-        for (int64_t i = 0; i < 2 * first; ++i) (void)dist(gen);
-        double* o = static_cast<double*>(out);
-        for (int64_t i = 0; i < count; ++i) {
-            const double im = dist(gen);
-            const double re = dist(gen);
-            o[2 * i] = re;
-            o[2 * i + 1] = im;
-        }
-    }
-}
-
 // window_coeffs (filter.cpp:43-56)
 std::vector<double> window_coeffs(double tlo, double thi, double blo, double bhi, int degree) {
     if (!(tlo < thi)) fail(CHEBFD_ERR_INVALID_ARGUMENT, "degenerate target interval");

@@ -151,6 +151,18 @@ def test_device_calls_fail_loudly_without_gpu():
         cf.Context(0)
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+def test_parallel_randomize_is_the_reference_stream(orc, cplx):
+    """chebfd_host_randomize (mt19937_64 jump-ahead + parallel polar method)
+    must equal the serial libstdc++ stream bit for bit, across chunk
+    boundaries and for row slices (distributed blocks)."""
+    dim, w = (1 << 20, 9) if not cplx else (1 << 19, 9)   # >= 2^23 normals: parallel path
+    full = orc.randomize(dim, w, 7, cplx)
+    assert bits(cf.host_randomize(dim, w, 7, cplx), full)
+    for r0, n in ((12345, 1000), (dim // 2 + 1, 777), (dim - 3, 3)):
+        assert bits(cf.host_randomize(dim, w, 7, cplx, r0, n), full[r0:r0 + n])
+
+
 def test_partition_plans_cover_rows_and_pair_up():
     spec = cf.LatticeSpec(4, 4, 8, disorder=0.5)
     for nranks in (1, 2, 3, 4):
