@@ -85,6 +85,19 @@ def main():
     json.dump(dict(lx=16, ly=16, iters=40, seed=6, lo=lo, hi=hi),
               open(os.path.join(HERE, "lanczos_g16.json"), "w"))
 
+    # automatic degree (choose_parameters) on a small TI slab
+    t6 = r.topological_insulator(6, 6, 6, disorder=0.5, seed=4)
+    rep = r.solve(t6, (-0.45, 0.45), degree=0, kernel="lanczos2", seed=3, dos_moments=600,
+                  dos_samples=16)
+    json.dump(dict(config="TI 6x6x6 slab V=0.5 seed=4, target [-0.45,0.45], N_S auto, degree "
+                          "auto (choose_parameters), lanczos2, seed 3, dos 600x16",
+                   converged=bool(rep["converged"]), iterations=rep["iterations"],
+                   degree=rep["degree"], n_search=rep["n_search"], sigma=rep["sigma"],
+                   eta=rep["eta"], n_target_estimate=rep["n_target_estimate"],
+                   bounds=[rep["bounds_lo"], rep["bounds_hi"]],
+                   accepted_values=sorted(rep["values"][rep["accepted"]].tolist())),
+              open(os.path.join(HERE, "ti6_auto_solve.json"), "w"), indent=1)
+
     r.set_threads(8)  # solve results do not depend on the thread count beyond rounding
     c1 = r.graphene(64, 64, disorder=0.1, seed=1)
     rep = r.solve(c1, (-0.13, 0.13), n_search=40, degree=500, kernel="lanczos2", seed=1)

@@ -195,3 +195,18 @@ def test_solve_config1_matches_reference(ctx):
     assert np.max(np.abs(acc - want)) <= 1e-10  # north_star: Ritz values within 1e-10
     assert np.all(rep.ritz.residual_norms[rep.ritz.accepted] <= 1e-10)
     assert abs(rep.weight_integral - 40.0) <= 0.4  # test_solver.cpp:256: integral = N_S (1%)
+
+
+def test_solve_automatic_degree_matches_reference(ctx):
+    """solve with degree = 0: the reference's degree rule (choose_parameters,
+    solver.cpp:130-136) on a TI slab; golden from the compiled reference."""
+    g = json.load(open(os.path.join(GOLDEN, "ti6_auto_solve.json")))
+    A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(6, 6, 6, disorder=0.5, seed=4))
+    rep = cf.solve(A, cf.SolverOptions(target=cf.Interval(-0.45, 0.45), degree=0, seed=3,
+                                       dos_moments=600, dos_samples=16))
+    assert rep.converged and rep.degree == g["degree"] and rep.n_search == g["n_search"]
+    assert rep.iterations == g["iterations"]
+    assert abs(rep.sigma - g["sigma"]) <= 1e-9 * g["sigma"]
+    acc = np.sort(rep.ritz.values[rep.ritz.accepted])
+    assert np.max(np.abs(acc - np.array(g["accepted_values"]))) <= 1e-10
+    assert set(rep.timings) == {"bounds", "dos", "design", "filter", "ortho", "rr"}
