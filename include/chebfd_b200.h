@@ -197,6 +197,35 @@ int chebfd_block_copy_columns(chebfd_block* dst, int64_t d0, const chebfd_block*
                               int64_t n);
 int chebfd_block_device_ptr(chebfd_block* b, void** ptr);
 
+/* ---- on-disk formats (matrix_market.cpp, block_vector.hpp:63-96) -------------- */
+/* Matrix Market coordinate reader (read_matrix_market, matrix_market.cpp:98-115):
+ * real / integer / complex fields, general / symmetric / hermitian storage
+ * (mirrored entries added, conjugated for hermitian), duplicates summed in file
+ * order, 1-based indices.  Host CSR out (ascending columns).  Call with
+ * offs == NULL to get kind / dim / nnz, then again with arrays of dim+1, nnz
+ * and nnz (x2 for complex) entries.  *hermitian = storage != general.
+ * Errors: CHEBFD_ERR_RUNTIME (banner, field, symmetry, size line, short file),
+ * CHEBFD_ERR_OUT_OF_RANGE (index outside [1, D]). */
+int chebfd_read_matrix_market(const char* path, int* kind, int64_t* dim, int64_t* nnz,
+                              int64_t* offs, int64_t* cols, void* vals, int* hermitian);
+/* write_matrix_market (matrix_market.cpp:63-95): lower triangle when hermitian
+ * != 0, 17 significant digits (exact round trip). */
+int chebfd_write_matrix_market(const char* path, int kind, int64_t dim, const int64_t* offs,
+                               const int64_t* cols, const void* vals, int hermitian);
+/* Read a Matrix Market file straight into a device SELL matrix (== read + from_csr). */
+int chebfd_matrix_from_matrix_market(chebfd_ctx* ctx, const char* path, chebfd_matrix** out);
+/* .cbfd block dumps (BlockVector::save/load): u32 magic 0x44464243 "CBFD",
+ * u64 D, u32 nb, u32 kind (0 real, 1 complex), D*nb row-major scalars.
+ * Raw host-buffer form; data == NULL on load reads only the header.
+ * Errors: CHEBFD_ERR_RUNTIME ("bad header", "scalar kind mismatch",
+ * "truncated payload", cannot open). */
+int chebfd_cbfd_save(const char* path, int kind, uint64_t dim, uint32_t width, const void* data);
+int chebfd_cbfd_load(const char* path, int* kind, uint64_t* dim, uint32_t* width, void* data);
+/* Device-block forms (single-GPU contexts; a distributed block gives
+ * CHEBFD_ERR_UNSUPPORTED).  load creates a block conforming to `a`. */
+int chebfd_block_save(const chebfd_block* b, const char* path);
+int chebfd_block_load(chebfd_matrix* a, const char* path, chebfd_block** out);
+
 /* ---- kernels (kernels.hpp) ---------------------------------------------------- */
 /* Y = (alpha A + beta I) X                                  kernels.hpp:45-69 */
 int chebfd_spmmvm(chebfd_matrix* a, chebfd_block* x, chebfd_block* y, double alpha, double beta);

@@ -18,6 +18,7 @@
 #include <string>
 #include <type_traits>
 #include <utility>
+#include <variant>
 #include <vector>
 
 #include "chebfd_b200.h"
@@ -143,6 +144,34 @@ inline SparseMatrix<Complex> topological_insulator(Context& ctx, const LatticeSp
     return SparseMatrix<Complex>(h);
 }
 
+// ---- Matrix Market (matrix_market.hpp) ---------------------------------------------------
+using MatrixVariant = std::variant<SparseMatrix<double>, SparseMatrix<Complex>>;
+
+// read_matrix_market (matrix_market.cpp:98-115), straight to a device matrix
+inline MatrixVariant read_matrix_market(Context& ctx, const std::string& path) {
+    chebfd_matrix* h = nullptr;
+    check(chebfd_matrix_from_matrix_market(ctx.get(), path.c_str(), &h));
+    chebfd_matrix_info i{};
+    const int rc = chebfd_matrix_get_info(h, &i);
+    if (rc != CHEBFD_OK) {
+        chebfd_matrix_destroy(h);
+        check(rc);
+    }
+    if (i.kind == CHEBFD_COMPLEX128) return MatrixVariant(std::in_place_index<1>, h);
+    return MatrixVariant(std::in_place_index<0>, h);
+}
+
+// write_matrix_market (matrix_market.cpp:63-95) of a host CSR
+template <class S>
+void write_matrix_market(const std::string& path, Index dim, const std::vector<Index>& row_offsets,
+                         const std::vector<Index>& col_indices, const std::vector<S>& values,
+                         bool hermitian = true) {
+    if (static_cast<Index>(row_offsets.size()) != dim + 1 || col_indices.size() != values.size())
+        throw std::invalid_argument("write_matrix_market: inconsistent CSR arrays");
+    check(chebfd_write_matrix_market(path.c_str(), kind_of<S>, dim, row_offsets.data(),
+                                     col_indices.data(), values.data(), hermitian ? 1 : 0));
+}
+
 // ---- device block vector -----------------------------------------------------------------
 template <class S>
 class BlockVector {
@@ -166,6 +195,13 @@ class BlockVector {
         return out;
     }
     void randomize(std::uint64_t seed) { check(chebfd_block_randomize(h_.get(), seed)); }
+    // BlockVector::save / load (block_vector.hpp:65-95), .cbfd format
+    void save(const std::string& path) const { check(chebfd_block_save(h_.get(), path.c_str())); }
+    static BlockVector load(const SparseMatrix<S>& a, const std::string& path) {
+        chebfd_block* h = nullptr;
+        check(chebfd_block_load(a.get(), path.c_str(), &h));
+        return BlockVector(h);
+    }
     chebfd_block* get() const { return h_.get(); }
 
   private:

@@ -356,6 +356,10 @@ class Ref:
         L.ref_solve.argtypes = [_vp, _vp, _vp, C.c_int, _vp, _vp, _vp, _vp]
         L.ref_intensity_model.argtypes = [_dbl, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp]
         L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_read_matrix_market.argtypes = [C.c_char_p, _vp, _vp]
+        L.ref_write_matrix_market.argtypes = [_vp, C.c_char_p, C.c_int]
+        L.ref_block_save.argtypes = [C.c_int, _i64, _i64, _vp, C.c_char_p]
+        L.ref_block_load.argtypes = [C.c_int, C.c_char_p, _vp, _vp, _vp]
         if threads is not None:
             L.ref_set_threads(threads)
 
@@ -545,6 +549,30 @@ class Ref:
         out = _dbl()
         self._chk(self.lib.ref_intensity_model(n_nzr, s_d, s_i, f_a, f_m, n_b, C.byref(out)))
         return out.value
+
+    # -- on-disk formats (matrix_market.cpp, block_vector.hpp:63-96) ------
+    def read_matrix_market(self, path):
+        """-> (RefMatrix, hermitian flag)"""
+        h, herm = _vp(), C.c_int()
+        self._chk(self.lib.ref_read_matrix_market(os.fsencode(path), C.byref(h), C.byref(herm)))
+        return RefMatrix(self, h), bool(herm.value)
+
+    def write_matrix_market(self, m, path, hermitian=True):
+        self._chk(self.lib.ref_write_matrix_market(m.h, os.fsencode(path), int(hermitian)))
+
+    def block_save(self, block, path):
+        a = np.ascontiguousarray(block)
+        kind = int(np.iscomplexobj(a))
+        self._chk(self.lib.ref_block_save(kind, a.shape[0], a.shape[1], _ptr(a), os.fsencode(path)))
+
+    def block_load(self, path, complex_=False):
+        d, w = _i64(), _i64()
+        self._chk(self.lib.ref_block_load(int(complex_), os.fsencode(path), C.byref(d), C.byref(w),
+                                          None))
+        out = np.empty((d.value, w.value), np.complex128 if complex_ else np.float64)
+        self._chk(self.lib.ref_block_load(int(complex_), os.fsencode(path), C.byref(d), C.byref(w),
+                                          _ptr(out)))
+        return out
 
 
 def ref_available():

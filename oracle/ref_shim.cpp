@@ -14,6 +14,7 @@
 #include <chebfd/filter.hpp>
 #include <chebfd/filter_design.hpp>
 #include <chebfd/kernels.hpp>
+#include <chebfd/matrix_market.hpp>
 #include <chebfd/models.hpp>
 #include <chebfd/parallel.hpp>
 #include <chebfd/solver.hpp>
@@ -554,6 +555,58 @@ int ref_intensity_model(double n_nzr, int s_d, int s_i, int f_a, int f_m, int n_
     return guard([&] {
         IntensityParams p{n_nzr, s_d, s_i, f_a, f_m};
         *out = intensity_model(p, n_b);
+    });
+}
+
+// ---- on-disk formats (matrix_market.cpp, block_vector.hpp:63-96) ----
+int ref_read_matrix_market(const char* path, void** out, int* hermitian) {
+    return guard([&] {
+        MatrixVariant v = read_matrix_market(path);
+        auto m = std::make_unique<RefMatrix>();
+        if (std::holds_alternative<SparseMatrix<double>>(v)) {
+            m->kind = 0;
+            m->r = std::get<SparseMatrix<double>>(std::move(v));
+            *hermitian = m->r.hermitian_flag();
+        } else {
+            m->kind = 1;
+            m->c = std::get<SparseMatrix<Complex>>(std::move(v));
+            *hermitian = m->c.hermitian_flag();
+        }
+        *out = m.release();
+    });
+}
+
+int ref_write_matrix_market(void* h, const char* path, int hermitian) {
+    return guard([&] {
+        with_matrix(h, [&](const auto& a) {
+            using M = std::decay_t<decltype(a)>;
+            M flagged(a.dim(), a.row_offsets(), a.col_indices(), a.values(), hermitian != 0);
+            write_matrix_market(path, flagged);
+        });
+    });
+}
+
+int ref_block_save(int kind, int64_t dim, int64_t width, const void* data, const char* path) {
+    return guard([&] {
+        if (kind == 0)
+            block_in<double>(data, dim, width).save(path);
+        else
+            block_in<Complex>(data, dim, width).save(path);
+    });
+}
+
+// loads as scalar kind `kind` (BlockVector<S>::load); data == nullptr: shape only
+int ref_block_load(int kind, const char* path, int64_t* dim, int64_t* width, void* data) {
+    return guard([&] {
+        auto take = [&](const auto& b) {
+            *dim = b.dim();
+            *width = b.width();
+            if (data) block_out(b, data);
+        };
+        if (kind == 0)
+            take(BlockVector<double>::load(path));
+        else
+            take(BlockVector<Complex>::load(path));
     });
 }
 

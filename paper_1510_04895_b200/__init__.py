@@ -14,7 +14,8 @@ from .api import (  # noqa: F401
     plan_all4, plan_complete_sends, plan_map_column, plan_partition, plan_sends,
     rayleigh_ritz, recurrence_step, solve, spmmvm, spmmvm_fused, svqb_orthonormalize,
     window_coeffs, DesignResult, choose_parameters, damping_factor, invert_search_margin,
-    optimize_degree, quality, host_randomize,
+    optimize_degree, quality, host_randomize, read_matrix_market, write_matrix_market,
+    save_block, load_block,
 )
 from ._lib import LIB_PATH, load  # noqa: F401
 

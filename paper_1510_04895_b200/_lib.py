@@ -102,6 +102,13 @@ _SIGS = {
     "chebfd_block_scale_columns": (_int, [_vp, _vp]),
     "chebfd_block_copy_columns": (_int, [_vp, _i64, _vp, _i64, _i64]),
     "chebfd_block_device_ptr": (_int, [_vp, _pp]),
+    "chebfd_read_matrix_market": (_int, [C.c_char_p, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "chebfd_write_matrix_market": (_int, [C.c_char_p, _int, _i64, _vp, _vp, _vp, _int]),
+    "chebfd_matrix_from_matrix_market": (_int, [_vp, C.c_char_p, _pp]),
+    "chebfd_cbfd_save": (_int, [C.c_char_p, _int, _u64, C.c_uint32, _vp]),
+    "chebfd_cbfd_load": (_int, [C.c_char_p, _vp, _vp, _vp, _vp]),
+    "chebfd_block_save": (_int, [_vp, C.c_char_p]),
+    "chebfd_block_load": (_int, [_vp, C.c_char_p, _pp]),
     "chebfd_spmmvm": (_int, [_vp, _vp, _vp, _dbl, _dbl]),
     "chebfd_spmmvm_fused": (_int, [_vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp]),
     "chebfd_recurrence_step": (_int, [_vp, _vp, _vp, _dbl, _dbl]),

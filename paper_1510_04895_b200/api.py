@@ -11,6 +11,7 @@ DomainError (ValueError), std::out_of_range -> OutOfRange (IndexError).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 from dataclasses import dataclass, field
 from typing import Optional
@@ -288,6 +289,13 @@ class SparseMatrix:
         return cls(ctx, h)
 
     @classmethod
+    def from_matrix_market(cls, ctx, path):
+        """read_matrix_market (matrix_market.cpp:98-115) straight to the device."""
+        h = C.c_void_p()
+        _check(_lib().chebfd_matrix_from_matrix_market(ctx._h, os.fsencode(path), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
     def graphene(cls, ctx, spec: LatticeSpec):
         h = C.c_void_p()
         s = spec._c()
@@ -404,6 +412,17 @@ class BlockVector:
         out = np.empty(self.shape, dtype=self.dtype)
         _check(_lib().chebfd_block_download(self._h, _ptr(out)))
         return out
+
+    def save(self, path):
+        """BlockVector::save (block_vector.hpp:65-78): .cbfd dump of the block."""
+        _check(_lib().chebfd_block_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, A: SparseMatrix, path) -> "BlockVector":
+        """BlockVector::load (block_vector.hpp:80-95) into a block conforming to A."""
+        h = C.c_void_p()
+        _check(_lib().chebfd_block_load(A._h, os.fsencode(path), C.byref(h)))
+        return cls(A, _handle=h)
 
     def copy_from(self, other: "BlockVector"):
         _check(_lib().chebfd_block_copy(self._h, other._h))
@@ -858,4 +877,55 @@ def host_randomize(dim: int, width: int, seed: int, complex_: bool = False, firs
     out = np.empty((rows, width), dtype=np.complex128 if complex_ else np.float64)
     _check(_lib().chebfd_host_randomize(int(complex_), seed, first_row * width, rows * width,
                                         _ptr(out)))
+    return out
+
+
+# ------------------------------------------------------------ on-disk formats --
+def read_matrix_market(path):
+    """Host CSR of a Matrix Market file (read_matrix_market, matrix_market.cpp:
+    98-115): returns (dim, offs, cols, vals, hermitian); vals complex128 for a
+    complex field, float64 for real / integer."""
+    lib, bpath = _lib(), os.fsencode(path)
+    kind, dim, nnz, herm = C.c_int(), C.c_int64(), C.c_int64(), C.c_int()
+    _check(lib.chebfd_read_matrix_market(bpath, C.byref(kind), C.byref(dim), C.byref(nnz),
+                                         None, None, None, C.byref(herm)))
+    offs = np.empty(dim.value + 1, np.int64)
+    cols = np.empty(nnz.value, np.int64)
+    vals = np.empty(nnz.value, np.complex128 if kind.value else np.float64)
+    _check(lib.chebfd_read_matrix_market(bpath, C.byref(kind), C.byref(dim), C.byref(nnz),
+                                         _ptr(offs), _ptr(cols), _ptr(vals), C.byref(herm)))
+    return dim.value, offs, cols, vals, bool(herm.value)
+
+
+def write_matrix_market(path, dim, row_offsets, col_indices, values, hermitian=True):
+    """write_matrix_market (matrix_market.cpp:63-95): lower triangle for a
+    Hermitian matrix, 17 significant digits."""
+    offs = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    cols = np.ascontiguousarray(col_indices, dtype=np.int64)
+    vals = np.ascontiguousarray(values)
+    kind = COMPLEX128 if np.iscomplexobj(vals) else REAL64
+    vals = vals.astype(np.complex128 if kind else np.float64, copy=False)
+    if len(offs) != dim + 1 or offs[-1] != len(cols) or len(cols) != len(vals):
+        raise InvalidArgument("write_matrix_market: inconsistent CSR arrays")
+    _check(_lib().chebfd_write_matrix_market(os.fsencode(path), kind, dim, _ptr(offs), _ptr(cols),
+                                             _ptr(vals), int(bool(hermitian))))
+
+
+def save_block(path, block: np.ndarray):
+    """.cbfd dump of a host D x nb block (BlockVector::save format)."""
+    a = np.ascontiguousarray(block)
+    if a.ndim != 2:
+        raise InvalidArgument("save_block: expects a 2-D block")
+    kind = COMPLEX128 if np.iscomplexobj(a) else REAL64
+    a = a.astype(np.complex128 if kind else np.float64, copy=False)
+    _check(_lib().chebfd_cbfd_save(os.fsencode(path), kind, a.shape[0], a.shape[1], _ptr(a)))
+
+
+def load_block(path) -> np.ndarray:
+    """Host block from a .cbfd file (BlockVector::load format)."""
+    lib, bpath = _lib(), os.fsencode(path)
+    kind, dim, width = C.c_int(), C.c_uint64(), C.c_uint32()
+    _check(lib.chebfd_cbfd_load(bpath, C.byref(kind), C.byref(dim), C.byref(width), None))
+    out = np.empty((dim.value, width.value), np.complex128 if kind.value else np.float64)
+    _check(lib.chebfd_cbfd_load(bpath, C.byref(kind), C.byref(dim), C.byref(width), _ptr(out)))
     return out

@@ -42,6 +42,19 @@ int main(int argc, char** argv) {
         threw = true;
     }
     EXPECT(threw);
+    // Matrix Market writer (host): 2x2 symmetric, lower triangle only
+    const std::string dir = argc > 2 ? argv[2] : ".";
+    const std::string mtx = dir + "/use_wrapper.mtx";
+    cb::write_matrix_market<double>(mtx, 2, {0, 2, 4}, {0, 1, 0, 1}, {2.0, -1.0, -1.0, 2.0});
+    if (std::FILE* f = std::fopen(mtx.c_str(), "r")) {
+        char buf[256] = {0};
+        const size_t got = std::fread(buf, 1, sizeof buf - 1, f);
+        std::fclose(f);
+        EXPECT(got > 0 && std::strcmp(buf, "%%MatrixMarket matrix coordinate real symmetric\n"
+                                           "2 2 3\n1 1 2\n2 1 -1\n2 2 2\n") == 0);
+    } else {
+        EXPECT(false);
+    }
     if (host_only) {
         threw = false;
         try {
@@ -75,6 +88,12 @@ int main(int argc, char** argv) {
         threw = true;  // test_core_linalg.cpp:157-164
     }
     EXPECT(threw);
+    // file round trips on the device path
+    auto V = cb::read_matrix_market(ctx, mtx);
+    EXPECT(V.index() == 0 && std::get<0>(V).dim() == 2 && std::get<0>(V).nnz() == 4);
+    X.save(dir + "/use_wrapper.cbfd");
+    auto Y = cb::BlockVector<cb::Complex>::load(A, dir + "/use_wrapper.cbfd");
+    EXPECT(Y.download() == X.download());
     std::printf("%s (device)\n", fails ? "FAILED" : "ok");
     return fails;
 }

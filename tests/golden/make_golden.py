@@ -5,7 +5,8 @@ into oracle/_ref/libchebfd_ref.so by oracle/Makefile).  The reference runs
 with one OpenMP thread so the chunked reductions are deterministic.  The
 fixtures are small and committed; the GPU box never needs the reference.
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # everything
+    python tests/golden/make_golden.py formats    # only tests/golden/formats/
 """
 import json
 import os
@@ -20,9 +21,26 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 
 
+def formats_golden(r):
+    """Matrix Market / .cbfd files written by the reference itself."""
+    d = os.path.join(HERE, "formats")
+    os.makedirs(d, exist_ok=True)
+    g = r.graphene(6, 5, disorder=0.3, seed=2)
+    r.write_matrix_market(g, os.path.join(d, "graphene_6x5_symmetric.mtx"), hermitian=True)
+    r.write_matrix_market(g, os.path.join(d, "graphene_6x5_general.mtx"), hermitian=False)
+    t = r.topological_insulator(2, 2, 3, disorder=0.4, seed=6)
+    r.write_matrix_market(t, os.path.join(d, "ti_2x2x3_hermitian.mtx"), hermitian=True)
+    r.block_save(r.randomize(30, 4, 5, False), os.path.join(d, "block_real_30x4.cbfd"))
+    r.block_save(r.randomize(12, 3, 6, True), os.path.join(d, "block_complex_12x3.cbfd"))
+
+
 def main():
     oracle.build()
     r = oracle.Ref(threads=1)
+    if sys.argv[1:] == ["formats"]:
+        formats_golden(r)
+        return
+    formats_golden(r)
     out = {}
 
     # --- models (models.cpp) ---------------------------------------------

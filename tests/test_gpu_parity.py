@@ -232,7 +232,8 @@ def test_cpp_dropin_layer_on_device(lib_built, tmp_path):
                         f"-L{os.path.dirname(lib_built)}", "-lchebfd_b200",
                         f"-Wl,-rpath,{os.path.dirname(lib_built)}"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
-    run = subprocess.run([str(out)], capture_output=True, text=True, timeout=120)
+    run = subprocess.run([str(out), "--device", str(tmp_path)], capture_output=True, text=True,
+                         timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
 
 

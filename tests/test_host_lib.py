@@ -52,7 +52,7 @@ def test_cpp_wrapper_header_compiles(lib_built, tmp_path):
                         "-o", str(out), f"-L{os.path.dirname(lib_built)}", "-lchebfd_b200",
                         f"-Wl,-rpath,{os.path.dirname(lib_built)}"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
-    run = subprocess.run([str(out), "--host-only"], capture_output=True, text=True)
+    run = subprocess.run([str(out), "--host-only", str(tmp_path)], capture_output=True, text=True)
     assert run.returncode == 0, run.stdout + run.stderr
 
 
