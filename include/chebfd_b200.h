@@ -78,10 +78,7 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count);
  * graphs, default 1); CHEBFD_OPT_OVERLAP (1 = overlap the halo exchange with
  * interior rows, default 1); CHEBFD_OPT_KERNEL (step kernel variant: 0 plain
  * register gathers, 1 TMA-staged SELL chunks with pre-scaled values; default 1). */
-/* CHEBFD_OPT_PLANE_ORDER: tile traversal of lattice matrices, 0 natural row
- * order, Y > 0: 2.5D blocking -- bands of Y lattice lines swept through all
- * planes of the partition before the next band. */
-enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3, CHEBFD_OPT_PLANE_ORDER = 4 };
+enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3 };
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */

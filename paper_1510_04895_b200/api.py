@@ -154,9 +154,8 @@ class Context:
         return ms.value
 
     def set_option(self, name: str, value):
-        """graphs (bool), overlap (bool), kernel ("gather" | "tma"),
-        plane_order (0 natural row order, Y > 0 bands of Y lattice lines)."""
-        code = {"graphs": 1, "overlap": 2, "kernel": 3, "plane_order": 4}[name]
+        """graphs (bool), overlap (bool), kernel ("gather" | "tma")."""
+        code = {"graphs": 1, "overlap": 2, "kernel": 3}[name]
         if name == "kernel" and isinstance(value, str):
             value = {"gather": 0, "tma": 1}[value]
         _check(_lib().chebfd_ctx_set_option(self._h, code, int(value)))

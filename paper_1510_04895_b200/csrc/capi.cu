@@ -592,8 +592,6 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->overlap = value != 0;
         else if (option == CHEBFD_OPT_KERNEL)
             c->kernel_variant = static_cast<int>(value);
-        else if (option == CHEBFD_OPT_PLANE_ORDER)
-            c->plane_order = static_cast<int>(value);
         else
             fail(CHEBFD_ERR_INVALID_ARGUMENT, "unknown option");
     });

@@ -157,7 +157,6 @@ struct FilterWorkspace {
 struct Context {
     int device = 0, rank = 0, nranks = 1, num_sms = 148;
     double l2_bytes = 126.0 * (1 << 20);
-    int plane_order = 0;  // tile order: 0 natural; Y > 0: 2.5D bands of Y lines swept through all planes
     cudaStream_t stream = nullptr;       // compute
     cudaStream_t comm_stream = nullptr;  // halo exchange
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;

@@ -231,9 +231,6 @@ struct StepParams {
     int nparts;
     int final_launch;
     unsigned* counter;
-    int64_t tiles_per_plane;  // > 0: visit tiles band-major (2.5D blocking) for L2 reuse
-    int64_t nplanes;
-    int64_t tiles_per_band;   // tiles of one plane visited before moving to the next plane
 };
 
 // Sum_j (a_rj * scale) * in[c_rj] over one row, in the row's stored order.
@@ -479,19 +476,8 @@ __global__ void __launch_bounds__(256, CFD_TMA_MINB) step_tma_kernel(const StepP
     const int64_t ntiles = row1 > row0 ? (cend - cbeg + NCH - 1) / NCH : 0;
     const int64_t* __restrict__ cptr = p.chunk_ptr;
 
-    // tile visiting order: natural, or (xy-tile, plane) with the plane index
-    // fastest so the z +- 1 neighbour rows a tile gathers are being read by
-    // concurrently running CTAs (L2 hits) instead of one plane (~1 GB) later
-    const int64_t tpp = p.tiles_per_plane, npl = p.nplanes, tpb = p.tiles_per_band;
-    auto order = [&](int64_t ti) {
-        if (tpp <= 0) return ti;
-        const int64_t sweep = tpb * npl;  // one band through every plane
-        const int64_t band = ti / sweep, rem = ti - band * sweep;
-        const int64_t z = rem / tpb;
-        return z * tpp + band * tpb + (rem - z * tpb);
-    };
-    auto issue = [&](int64_t ti, int buf) {
-        const int64_t c0 = cbeg + order(ti) * NCH;
+    auto issue = [&](int64_t tile, int buf) {
+        const int64_t c0 = cbeg + tile * NCH;
         const int64_t c1e = min(c0 + NCH, cend);
         const int64_t s0 = cptr[c0], s1 = cptr[c1e];
         const unsigned n = static_cast<unsigned>(s1 - s0);
@@ -562,7 +548,7 @@ __global__ void __launch_bounds__(256, CFD_TMA_MINB) step_tma_kernel(const StepP
     for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
         const int buf = k & 1;
         if (t == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
-        const int64_t c0 = cbeg + order(tile) * NCH;
+        const int64_t c0 = cbeg + tile * NCH;
         const int64_t c1e = min(c0 + NCH, cend);
         const int64_t sbase = cptr[c0];
         // fast tile: all chunks full, width == MAXW, tile fully inside [row0, row1)
@@ -873,23 +859,6 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         p.nparts = s.partial_base + grid;
         p.final_launch = s.final_launch ? 1 : 0;
         p.counter = ctx.counter.as<unsigned>();
-        // plane-major traversal when one plane of the gathered block outgrows
-        // ~1/8 of L2 and the launch covers whole planes made of whole tiles
-        p.tiles_per_plane = 0;
-        p.nplanes = 0;
-        p.tiles_per_band = 0;
-        if (tma && a.plane_rows > 0 && a.plane_rows % TR == 0 && s.row0 % a.plane_rows == 0 &&
-            (s.row1 - s.row0) % a.plane_rows == 0 && (s.row1 - s.row0) / a.plane_rows > 1 &&
-            ctx.plane_order > 0) {
-            // band = plane_order lines (y-rows of the plane); whole tiles per band
-            int64_t band_rows = a.line_rows > 0 ? ctx.plane_order * a.line_rows : a.plane_rows;
-            band_rows = std::min<int64_t>(band_rows, a.plane_rows);
-            if (band_rows % TR == 0 && a.plane_rows % band_rows == 0) {
-                p.tiles_per_plane = a.plane_rows / TR;
-                p.nplanes = (s.row1 - s.row0) / a.plane_rows;
-                p.tiles_per_band = band_rows / TR;
-            }
-        }
         if (nrows > 0) {
             kernel<<<grid, g.threads, smem, st>>>(p);
             CFD_CUDA(cudaGetLastError());

@@ -235,20 +235,3 @@ def test_cpp_dropin_layer_on_device(lib_built, tmp_path):
     run = subprocess.run([str(out), "--device", str(tmp_path)], capture_output=True, text=True,
                          timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
-
-
-@pytest.mark.parametrize("order", [1, 2, 8, 0])
-def test_band_traversal_bitexact(ctx, orc, order):
-    """2.5D band tile order (C4 locality) must not change any bit."""
-    ctx.set_option("plane_order", order)
-    try:
-        A, c = ti(ctx, orc, (8, 8, 6))
-        p = cf.make_filter((-0.2, 0.3), (-5.6, 5.6), 12, "lanczos2")
-        x0 = orc.randomize(c.dim, 16, 4, True)
-        X = block(A, x0)
-        mom = cf.apply_filter(A, X, p, want_moments=True)
-        xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
-        assert bits_equal(X.to_numpy(), xr)
-        assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
-    finally:
-        ctx.set_option("plane_order", 0)

@@ -22,11 +22,9 @@ def main():
     ap.add_argument("--model", default="ti", choices=["ti", "graphene"])
     ap.add_argument("--moments", action="store_true")
     ap.add_argument("--lz", type=int, default=0, help="TI z extent (default = lattice)")
-    ap.add_argument("--plane-order", type=int, default=0)
     args = ap.parse_args()
     ctx = cf.Context(0)
     ctx.set_option("kernel", args.kernel)
-    ctx.set_option("plane_order", args.plane_order)
     L = args.lattice
     if args.model == "ti":
         A = cf.SparseMatrix.topological_insulator(
