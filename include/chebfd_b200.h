@@ -282,6 +282,34 @@ int chebfd_kpm_dos(chebfd_matrix* a, double bounds_lo, double bounds_hi, int ord
 int chebfd_dos_count(const double* mu, int order, double bounds_lo, double bounds_hi, double lo,
                      double hi, double* out);
 
+/* ---- bench front end (bench.hpp / bench.cpp) ------------------------------------- */
+/* BenchPoint (bench.hpp:49-58): model flops and traffic (bench.cpp:28-34, S_i = 4)
+ * over the measured seconds per filter application. */
+typedef struct {
+    int n_b;
+    double seconds;    /* per apply_filter (device events, incl. the y = x copy as timed there) */
+    double flops;      /* per_row_flops * D * n_b * degree */
+    double gflops;
+    double gbs_proxy;  /* model traffic / seconds */
+    double intensity;  /* I(n_b) */
+    double roofline;   /* P* = I(n_b) * b, Gflop/s */
+    double efficiency; /* gflops / roofline */
+} chebfd_bench_point;
+/* bandwidth_probe_min_bytes (bench.cpp:42): 8 x the last-level cache (the GPU's L2). */
+int chebfd_bandwidth_probe_min_bytes(chebfd_ctx* ctx, uint64_t* out);
+/* bandwidth_probe (bench.cpp:44-67) on HBM: read-only streaming reduction over
+ * size_bytes (>= the minimum, else CHEBFD_ERR_INVALID_ARGUMENT), max(reps, 5)
+ * sweeps timed with CUDA events, median GB/s. */
+int chebfd_bandwidth_probe(chebfd_ctx* ctx, uint64_t size_bytes, int reps, double* gbs);
+/* bench_filter (bench.cpp:71-126): window = central 10 % of lanczos_bounds(a, 30),
+ * Lanczos-2, start block randomize(7); per block size one untimed application
+ * (kernel loading + graph capture), then the reference's protocol: one timed
+ * warm-up application, repeated (y = x; apply) until >= 0.1 s.  bandwidth_gbs <= 0 runs the probe;
+ * *bandwidth_used receives b.  points[n_sizes].  Errors (invalid_argument):
+ * degree < 16, empty sweep, n_b < 1. */
+int chebfd_bench_filter(chebfd_matrix* a, const int* block_sizes, int n_sizes, int degree,
+                        double bandwidth_gbs, chebfd_bench_point* points, double* bandwidth_used);
+
 /* ---- filter design (filter_design.hpp / filter_design.cpp) ------------------------ */
 typedef struct {
     int np_opt;              /* optimal degree N_p */

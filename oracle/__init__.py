@@ -360,6 +360,7 @@ class Ref:
         L.ref_write_matrix_market.argtypes = [_vp, C.c_char_p, C.c_int]
         L.ref_block_save.argtypes = [C.c_int, _i64, _i64, _vp, C.c_char_p]
         L.ref_block_load.argtypes = [C.c_int, C.c_char_p, _vp, _vp, _vp]
+        L.ref_bench_filter.argtypes = [_vp, _vp, C.c_int, C.c_int, _dbl, _vp]
         if threads is not None:
             L.ref_set_threads(threads)
 
@@ -572,6 +573,14 @@ class Ref:
         out = np.empty((d.value, w.value), np.complex128 if complex_ else np.float64)
         self._chk(self.lib.ref_block_load(int(complex_), os.fsencode(path), C.byref(d), C.byref(w),
                                           _ptr(out)))
+        return out
+
+    def bench_filter(self, m, sizes, degree, bandwidth):
+        """-> (n, 8) rows: n_b, seconds, flops, gflops, gbs_proxy, intensity, roofline,
+        efficiency (bench.cpp:71-126)"""
+        sz = np.ascontiguousarray(sizes, dtype=np.int32)
+        out = np.zeros((len(sz), 8))
+        self._chk(self.lib.ref_bench_filter(m.h, _ptr(sz), len(sz), degree, bandwidth, _ptr(out)))
         return out
 
 

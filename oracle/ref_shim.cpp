@@ -610,4 +610,21 @@ int ref_block_load(int kind, const char* path, int64_t* dim, int64_t* width, voi
     });
 }
 
+// ---- bench front end (bench.cpp:71-126); out[8 * k] = n_b, seconds, flops, gflops,
+// gbs_proxy, intensity, roofline, efficiency of point k
+int ref_bench_filter(void* h, const int* sizes, int n, int degree, double bandwidth, double* out) {
+    return guard([&] {
+        with_matrix(h, [&](const auto& a) {
+            const BenchReport rep =
+                bench_filter(a, std::vector<int>(sizes, sizes + n), degree, bandwidth);
+            for (size_t k = 0; k < rep.points.size(); ++k) {
+                const BenchPoint& p = rep.points[k];
+                const double row[8] = {double(p.n_b), p.seconds,   p.flops,     p.gflops,
+                                       p.gbs_proxy,   p.intensity, p.roofline, p.efficiency};
+                std::memcpy(out + 8 * k, row, sizeof row);
+            }
+        });
+    });
+}
+
 }  // extern "C"

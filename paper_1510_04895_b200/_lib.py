@@ -46,6 +46,11 @@ class chebfd_design(C.Structure):
                 ("below_recommended_search_space", _int)]
 
 
+class chebfd_bench_point(C.Structure):
+    _fields_ = [("n_b", _int), ("seconds", _dbl), ("flops", _dbl), ("gflops", _dbl),
+                ("gbs_proxy", _dbl), ("intensity", _dbl), ("roofline", _dbl), ("efficiency", _dbl)]
+
+
 class chebfd_solver_options(C.Structure):
     _fields_ = [("target_lo", _dbl), ("target_hi", _dbl), ("epsilon", _dbl), ("n_search", _int),
                 ("degree", _int), ("kernel", _int), ("kernel_mu", _int), ("max_iters", _int),
@@ -102,6 +107,9 @@ _SIGS = {
     "chebfd_block_scale_columns": (_int, [_vp, _vp]),
     "chebfd_block_copy_columns": (_int, [_vp, _i64, _vp, _i64, _i64]),
     "chebfd_block_device_ptr": (_int, [_vp, _pp]),
+    "chebfd_bandwidth_probe_min_bytes": (_int, [_vp, C.POINTER(_u64)]),
+    "chebfd_bandwidth_probe": (_int, [_vp, _u64, _int, C.POINTER(_dbl)]),
+    "chebfd_bench_filter": (_int, [_vp, _vp, _int, _int, _dbl, _vp, C.POINTER(_dbl)]),
     "chebfd_read_matrix_market": (_int, [C.c_char_p, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "chebfd_write_matrix_market": (_int, [C.c_char_p, _int, _i64, _vp, _vp, _vp, _int]),
     "chebfd_matrix_from_matrix_market": (_int, [_vp, C.c_char_p, _pp]),

@@ -928,3 +928,74 @@ def load_block(path) -> np.ndarray:
     out = np.empty((dim.value, width.value), np.complex128 if kind.value else np.float64)
     _check(lib.chebfd_cbfd_load(bpath, C.byref(kind), C.byref(dim), C.byref(width), _ptr(out)))
     return out
+
+
+# ------------------------------------------------------------ bench front end --
+@dataclass
+class BenchPoint:
+    """bench.hpp:49-58"""
+    n_b: int
+    seconds: float
+    flops: float
+    gflops: float
+    gbs_proxy: float
+    intensity: float
+    roofline: float
+    efficiency: float
+
+
+@dataclass
+class BenchReport:
+    """bench.hpp:60-66; to_json() gives bench_report.json's schema (chebfd.cpp:336-357)."""
+    points: list
+    bandwidth_gbs: float
+    degree: int
+    dim: int
+    traffic_overhead: str = "not measured"  # hardware counters: see profiles/ (ncu)
+
+    def to_json(self):
+        return {"bandwidth_gbs": self.bandwidth_gbs, "degree": self.degree, "dim": self.dim,
+                "traffic_overhead": self.traffic_overhead,
+                "points": [{"n_b": p.n_b, "seconds": p.seconds, "flops": p.flops,
+                            "gflops": p.gflops, "gbs_proxy": p.gbs_proxy,
+                            "intensity": p.intensity, "roofline_gflops": p.roofline,
+                            "efficiency": p.efficiency} for p in self.points]}
+
+    def table(self):
+        """The CLI's text table (chebfd.cpp:329-343)."""
+        lines = [f"bandwidth: {self.bandwidth_gbs:g} GB/s   traffic overhead: "
+                 f"{self.traffic_overhead}",
+                 "  n_b   Gflop/s      GB/s  I(n_b)    P*(Gflop/s)  efficiency"]
+        for p in self.points:
+            lines.append(f"{p.n_b:5d} {p.gflops:9.3f} {p.gbs_proxy:9.3f} {p.intensity:7.4f} "
+                         f"{p.roofline:14.3f} {p.efficiency:11.3f}")
+        return "\n".join(lines)
+
+
+def bandwidth_probe_min_bytes(ctx: Context) -> int:
+    """8 x the GPU's L2 (bench.cpp:42 uses 8 x the LLC)."""
+    out = C.c_uint64()
+    _check(_lib().chebfd_bandwidth_probe_min_bytes(ctx._h, C.byref(out)))
+    return out.value
+
+
+def bandwidth_probe(ctx: Context, size_bytes: Optional[int] = None, reps: int = 5) -> float:
+    """bandwidth_probe (bench.cpp:44-67) on HBM: median GB/s of read-only sweeps."""
+    if size_bytes is None:
+        size_bytes = bandwidth_probe_min_bytes(ctx)
+    out = C.c_double()
+    _check(_lib().chebfd_bandwidth_probe(ctx._h, int(size_bytes), int(reps), C.byref(out)))
+    return out.value
+
+
+def bench_filter(A: SparseMatrix, block_sizes=(1, 2, 4, 8, 16, 32), degree: int = 100,
+                 bandwidth_gbs: float = 0.0) -> BenchReport:
+    """bench_filter (bench.cpp:71-126) on the device."""
+    sizes = np.ascontiguousarray(list(block_sizes), dtype=np.int32)
+    pts = (L.chebfd_bench_point * max(len(sizes), 1))()
+    bw = C.c_double()
+    _check(_lib().chebfd_bench_filter(A._h, _ptr(sizes), len(sizes), int(degree),
+                                      float(bandwidth_gbs), pts, C.byref(bw)))
+    points = [BenchPoint(*(getattr(pts[i], f) for f, _ in L.chebfd_bench_point._fields_))
+              for i in range(len(sizes))]
+    return BenchReport(points=points, bandwidth_gbs=bw.value, degree=int(degree), dim=A.dim())

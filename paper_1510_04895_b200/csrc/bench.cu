@@ -1,0 +1,226 @@
+// Bench front end: bench_filter's protocol and report
+// (bench.cpp:71-126, bench.hpp:36-76) on the device, with the paper's
+// read-only streaming bandwidth probe as the roofline's b (bench.cpp:44-67,
+// PAPER.md:780-781) run on HBM instead of host DRAM.
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "capi_common.hpp"
+
+namespace cfd {
+
+namespace {
+
+// 32-byte non-coherent streaming load (LDG.E.ENL2.256 on sm_100a)
+__device__ __forceinline__ double4 ld256(const double* p) {
+    double4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// read-only streaming reduction: 4 independent 32-byte loads in flight per
+// thread per iteration, one partial per thread written only if it is NaN (the
+// data never is) so the loads cannot be elided and no store traffic is added
+__global__ void __launch_bounds__(512) probe_read_kernel(const double* __restrict__ p, size_t n4,
+                                                         double* __restrict__ sink) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (; i + 3 * stride < n4; i += 4 * stride) {
+        const double4 v0 = ld256(p + 4 * i);
+        const double4 v1 = ld256(p + 4 * (i + stride));
+        const double4 v2 = ld256(p + 4 * (i + 2 * stride));
+        const double4 v3 = ld256(p + 4 * (i + 3 * stride));
+        a0 += (v0.x + v0.y) + (v0.z + v0.w);
+        a1 += (v1.x + v1.y) + (v1.z + v1.w);
+        a2 += (v2.x + v2.y) + (v2.z + v2.w);
+        a3 += (v3.x + v3.y) + (v3.z + v3.w);
+    }
+    for (; i < n4; i += stride) {
+        const double4 v = ld256(p + 4 * i);
+        a0 += (v.x + v.y) + (v.z + v.w);
+    }
+    const double acc = (a0 + a1) + (a2 + a3);
+    if (acc != acc) sink[blockIdx.x] = acc;
+}
+
+__global__ void probe_fill_kernel(double* __restrict__ p, size_t n) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        p[i] = 1.0 + 1e-9 * static_cast<double>(i % 1024);  // bench.cpp:52
+}
+
+void ok(int rc) {
+    if (rc != CHEBFD_OK) throw Error(rc, g_last_error);
+}
+
+struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    EventPair() {
+        CFD_CUDA(cudaEventCreate(&a));
+        CFD_CUDA(cudaEventCreate(&b));
+    }
+    ~EventPair() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    double seconds(cudaStream_t st) const {
+        CFD_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        CFD_CUDA(cudaEventElapsedTime(&ms, a, b));
+        (void)st;
+        return 1e-3 * static_cast<double>(ms);
+    }
+};
+
+struct BlockDel {
+    void operator()(chebfd_block* b) const { chebfd_block_destroy(b); }
+};
+using BlockPtr = std::unique_ptr<chebfd_block, BlockDel>;
+
+BlockPtr new_block(chebfd_matrix* a, int64_t nb) {
+    chebfd_block* h = nullptr;
+    ok(chebfd_block_create(a, nb, &h));
+    return BlockPtr(h);
+}
+
+// bench.cpp:28-34 (the IntensityParams conventions of scalar.hpp / bench.hpp)
+struct Params {
+    double n_nzr;
+    int s_d, s_i, f_a, f_m;
+};
+double per_row_flops(const Params& p) {
+    return p.n_nzr * (p.f_a + p.f_m) + std::ceil(9.0 * p.f_a / 2.0) + std::ceil(11.0 * p.f_m / 2.0);
+}
+double per_row_bytes(const Params& p, int n_b) { return p.n_nzr / n_b * (p.s_d + p.s_i) + 5.0 * p.s_d; }
+
+}  // namespace
+
+size_t probe_min_bytes(const Context& c) { return 8 * static_cast<size_t>(c.l2_bytes); }
+
+// bandwidth_probe (bench.cpp:44-67): median GB/s of >= 5 read-only sweeps
+double bandwidth_probe(Context& c, size_t size_bytes, int reps) {
+    reps = std::max(reps, 5);
+    if (size_bytes < probe_min_bytes(c))
+        fail(CHEBFD_ERR_INVALID_ARGUMENT, "bandwidth_probe: array must be at least 8x the LLC size");
+    const size_t n = size_bytes / sizeof(double);
+    DeviceBuffer buf;
+    buf.ensure(n * sizeof(double) + 32);
+    DeviceBuffer sink;
+    sink.ensure(sizeof(double) * 4096);
+    const int fill_grid = c.num_sms * 8;
+    probe_fill_kernel<<<fill_grid, 256, 0, c.stream>>>(buf.as<double>(), n);
+    CFD_CUDA(cudaGetLastError());
+    const size_t n4 = n / 4;  // whole 32-byte units (a trailing remainder is not read)
+    const int grid = c.num_sms * 4;
+    EventPair ev;
+    std::vector<double> rates(static_cast<size_t>(reps));
+    for (int r = 0; r < reps; ++r) {
+        CFD_CUDA(cudaEventRecord(ev.a, c.stream));
+        probe_read_kernel<<<grid, 512, 0, c.stream>>>(buf.as<double>(), n4, sink.as<double>());
+        CFD_CUDA(cudaGetLastError());
+        CFD_CUDA(cudaEventRecord(ev.b, c.stream));
+        const double dt = ev.seconds(c.stream);
+        c.launches += 1;
+        rates[static_cast<size_t>(r)] = static_cast<double>(n4 * 32) / dt / 1e9;
+    }
+    std::nth_element(rates.begin(), rates.begin() + reps / 2, rates.end());
+    return rates[static_cast<size_t>(reps / 2)];
+}
+
+}  // namespace cfd
+
+using namespace cfd;
+
+extern "C" {
+
+int chebfd_bandwidth_probe_min_bytes(chebfd_ctx* ctx, uint64_t* out) {
+    return guard([&] { *out = probe_min_bytes(*reinterpret_cast<Context*>(ctx)); });
+}
+
+int chebfd_bandwidth_probe(chebfd_ctx* ctx, uint64_t size_bytes, int reps, double* gbs) {
+    return guard([&] {
+        *gbs = bandwidth_probe(*reinterpret_cast<Context*>(ctx), static_cast<size_t>(size_bytes),
+                               reps);
+    });
+}
+
+// bench_filter (bench.cpp:71-126)
+int chebfd_bench_filter(chebfd_matrix* a, const int* block_sizes, int n_sizes, int degree,
+                        double bandwidth_gbs, chebfd_bench_point* points, double* bandwidth_used) {
+    return guard([&] {
+        Matrix& m = *reinterpret_cast<Matrix*>(a);
+        Context& c = *m.ctx;
+        if (degree < 16) fail(CHEBFD_ERR_INVALID_ARGUMENT, "bench_filter: degree must be >= 16");
+        if (n_sizes <= 0 || !block_sizes)
+            fail(CHEBFD_ERR_INVALID_ARGUMENT, "bench_filter: empty block-size sweep");
+        for (int s = 0; s < n_sizes; ++s)
+            if (block_sizes[s] < 1)
+                fail(CHEBFD_ERR_INVALID_ARGUMENT, "bench_filter: block size must be >= 1");
+        const double bw =
+            bandwidth_gbs > 0.0 ? bandwidth_gbs : bandwidth_probe(c, probe_min_bytes(c), 5);
+        if (bandwidth_used) *bandwidth_used = bw;
+
+        // window = the central 10% of the Lanczos bounds, Lanczos-2 kernel
+        double blo = 0.0, bhi = 0.0;
+        ok(chebfd_lanczos_bounds(a, 30, 1, &blo, &bhi));
+        const double hw = 0.5 * (bhi - blo), ctr = 0.5 * (blo + bhi);
+        std::vector<double> comb(static_cast<size_t>(degree) + 1);
+        double alpha = 0.0, beta = 0.0;
+        ok(chebfd_make_filter(ctr - 0.05 * hw, ctr + 0.05 * hw, blo, bhi, degree,
+                              CHEBFD_KERNEL_LANCZOS, 2, comb.data(), &alpha, &beta));
+
+        const double dim = static_cast<double>(m.part.dim);
+        const Params p{m.part.dim ? static_cast<double>(m.nnz_global) / dim : 0.0, m.kind ? 16 : 8,
+                       4, m.kind ? 2 : 1, m.kind ? 6 : 1};
+        if (!(p.n_nzr > 0.0))
+            fail(CHEBFD_ERR_INVALID_ARGUMENT, "intensity_model: N_nzr must be positive");
+        EventPair ev;
+        for (int s = 0; s < n_sizes; ++s) {
+            const int nb = block_sizes[s];
+            BlockPtr x = new_block(a, nb);
+            ok(chebfd_block_randomize(x.get(), 7));
+            // GPU-only extra warm-up, untimed: the first application of a block
+            // width loads its kernels (lazy module loading, ~0.1 s) and
+            // captures its CUDA graph -- one-time costs the host reference
+            // does not have
+            BlockPtr y = new_block(a, nb);
+            ok(chebfd_block_copy(y.get(), x.get()));
+            ok(chebfd_apply_filter(a, y.get(), comb.data(), degree, alpha, beta, nullptr));
+            // then the reference's protocol: warm up and size the repetition
+            // count off one (timed) application
+            ok(chebfd_block_copy(y.get(), x.get()));
+            CFD_CUDA(cudaEventRecord(ev.a, c.stream));
+            ok(chebfd_apply_filter(a, y.get(), comb.data(), degree, alpha, beta, nullptr));
+            CFD_CUDA(cudaEventRecord(ev.b, c.stream));
+            double dt = ev.seconds(c.stream);
+            int runs = 1;
+            if (dt < 0.1) {
+                runs = static_cast<int>(std::ceil(0.1 / std::max(dt, 1e-6)));
+                CFD_CUDA(cudaEventRecord(ev.a, c.stream));
+                for (int r = 0; r < runs; ++r) {  // y = x; apply_filter(y) -- as timed there
+                    ok(chebfd_block_copy(y.get(), x.get()));
+                    ok(chebfd_apply_filter(a, y.get(), comb.data(), degree, alpha, beta, nullptr));
+                }
+                CFD_CUDA(cudaEventRecord(ev.b, c.stream));
+                dt = ev.seconds(c.stream);
+            }
+            chebfd_bench_point& pt = points[s];
+            pt.n_b = nb;
+            pt.seconds = dt / runs;
+            pt.flops = per_row_flops(p) * dim * nb * degree;
+            pt.gflops = pt.flops / pt.seconds / 1e9;
+            const double traffic = per_row_bytes(p, nb) * dim * nb * degree;
+            pt.gbs_proxy = traffic / pt.seconds / 1e9;
+            pt.intensity = per_row_flops(p) / per_row_bytes(p, nb);
+            pt.roofline = pt.intensity * bw;
+            pt.efficiency = pt.gflops / pt.roofline;
+        }
+    });
+}
+
+}  // extern "C"

@@ -7,6 +7,7 @@ fixtures are small and committed; the GPU box never needs the reference.
 
     python tests/golden/make_golden.py            # everything
     python tests/golden/make_golden.py formats    # only tests/golden/formats/
+    python tests/golden/make_golden.py bench      # only bench_filter.json
 """
 import json
 import os
@@ -34,13 +35,30 @@ def formats_golden(r):
     r.block_save(r.randomize(12, 3, 6, True), os.path.join(d, "block_complex_12x3.cbfd"))
 
 
+def bench_golden(r):
+    """bench_filter's model fields (timing-independent) from the reference."""
+    out = {}
+    for name, m, sizes in (("graphene_32x32", r.graphene(32, 32, disorder=0.2, seed=3), [1, 3, 8]),
+                           ("ti_4x4x4", r.topological_insulator(4, 4, 4, disorder=0.5, seed=2),
+                            [1, 4])):
+        rows = r.bench_filter(m, sizes, 16, 1000.0)
+        out[name] = dict(sizes=sizes, degree=16, bandwidth=1000.0,
+                         flops=rows[:, 2].tolist(), intensity=rows[:, 5].tolist(),
+                         roofline=rows[:, 6].tolist())
+    json.dump(out, open(os.path.join(HERE, "bench_filter.json"), "w"), indent=1)
+
+
 def main():
     oracle.build()
     r = oracle.Ref(threads=1)
     if sys.argv[1:] == ["formats"]:
         formats_golden(r)
         return
+    if sys.argv[1:] == ["bench"]:
+        bench_golden(r)
+        return
     formats_golden(r)
+    bench_golden(r)
     out = {}
 
     # --- models (models.cpp) ---------------------------------------------
