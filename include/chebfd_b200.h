@@ -78,7 +78,11 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count);
  * graphs, default 1); CHEBFD_OPT_OVERLAP (1 = overlap the halo exchange with
  * interior rows, default 1); CHEBFD_OPT_KERNEL (step kernel variant: 0 plain
  * register gathers, 1 TMA-staged SELL chunks with pre-scaled values; default 1). */
-enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3 };
+/* CHEBFD_OPT_SLAB_UNITS (step kernels sweep the block in column slabs of at
+ * most this many 16-byte units; 0 = 256, the measured best -- narrower slabs
+ * re-read the matrix per slab).  Changing any option drops captured filters. */
+enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
+       CHEBFD_OPT_SLAB_UNITS = 5 };
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */

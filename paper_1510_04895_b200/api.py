@@ -154,8 +154,9 @@ class Context:
         return ms.value
 
     def set_option(self, name: str, value):
-        """graphs (bool), overlap (bool), kernel ("gather" | "tma")."""
-        code = {"graphs": 1, "overlap": 2, "kernel": 3}[name]
+        """graphs (bool), overlap (bool), kernel ("gather" | "tma"),
+        slab_units (int, 0 = 256)."""
+        code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5}[name]
         if name == "kernel" and isinstance(value, str):
             value = {"gather": 0, "tma": 1}[value]
         _check(_lib().chebfd_ctx_set_option(self._h, code, int(value)))

@@ -586,12 +586,18 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count) {
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
     return guard([&] {
         Context* c = reinterpret_cast<Context*>(ctx);
+        // captured filters bake in the kernel choices: drop them all
+        ctx_sync(*c);
+        for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+        c->graphs.clear();
         if (option == CHEBFD_OPT_GRAPHS)
             c->use_graphs = value != 0;
         else if (option == CHEBFD_OPT_OVERLAP)
             c->overlap = value != 0;
         else if (option == CHEBFD_OPT_KERNEL)
             c->kernel_variant = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_SLAB_UNITS)
+            c->slab_units = static_cast<int>(value);
         else
             fail(CHEBFD_ERR_INVALID_ARGUMENT, "unknown option");
     });

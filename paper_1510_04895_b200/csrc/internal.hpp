@@ -167,6 +167,7 @@ struct Context {
     bool use_graphs = true, overlap = true;
     int kernel_variant = 1;  // step kernel: 0 register gathers, 1 TMA-staged matrix chunks
     int64_t launches = 0;
+    int slab_units = 0;   // step kernel column-slab width in 16-byte units (0: up to 256)
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
     DeviceBuffer partials;   // per-block partial sums
     DeviceBuffer counter;    // last-block-done ticket (uint32), self-resetting

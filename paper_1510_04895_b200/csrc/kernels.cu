@@ -790,9 +790,10 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     auto kernel = tma ? step_tma_kernel<CPLX, T, KIND, DMODE, MW>
                       : step_kernel<CPLX, T, KIND, DMODE, 0>;
     int used_total = 0;
-    // column slabs of at most 256 units (one CTA row-group spans a slab)
-    for (int u0 = 0; u0 < units; u0 += 256) {
-        const int us = std::min(256, units - u0);
+    // column slabs of at most `slab` units (one CTA row-group spans a slab)
+    const int slab = ctx.slab_units > 0 ? std::min(ctx.slab_units, 256) : 256;
+    for (int u0 = 0; u0 < units; u0 += slab) {
+        const int us = std::min(slab, units - u0);
         Geometry g = tma ? geometry_pow2(us) : geometry(us);
         const int TR = std::max(32, g.R);
         const size_t stage = tma ? 2 * static_cast<size_t>(MW) * TR : 0;
@@ -865,8 +866,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
             ctx.launches++;
         }
         used_total = grid;
-        if (units > 256 && NDOT > 0 && !s.final_launch)
-            fail(CHEBFD_ERR_UNSUPPORTED, "split dot launches need width <= 256 units");
+        if (units > slab && NDOT > 0 && !s.final_launch)
+            fail(CHEBFD_ERR_UNSUPPORTED, "split dot launches need a single column slab");
     }
     if (s.grid_used) *s.grid_used = used_total;
 }

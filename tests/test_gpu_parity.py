@@ -235,3 +235,32 @@ def test_cpp_dropin_layer_on_device(lib_built, tmp_path):
     run = subprocess.run([str(out), "--device", str(tmp_path)], capture_output=True, text=True,
                          timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
+
+
+def test_set_option_invalidates_captured_filters(ctx, orc):
+    """Options change which kernels a filter launches; a graph captured before
+    the change must not be replayed after it (results stay bit-exact)."""
+    A, c = ti(ctx, orc, (4, 4, 6))
+    p = cf.make_filter((-0.2, 0.3), (-5.6, 5.6), 12, "lanczos2")
+    x0 = orc.randomize(c.dim, 8, 4, True)
+    xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=False)
+    X = block(A, x0)
+
+    def run():
+        X.upload(x0)
+        before = ctx.launch_count
+        cf.apply_filter(A, X, p)
+        assert bits_equal(X.to_numpy(), xr)
+        return ctx.launch_count - before
+
+    d0 = run()
+    assert run() == d0  # replay of the captured graph
+    try:
+        ctx.set_option("slab_units", 2)  # 8 complex columns -> 4 column slabs per step
+        assert run() > d0
+        ctx.set_option("kernel", "gather")
+        run()
+    finally:
+        ctx.set_option("slab_units", 0)
+        ctx.set_option("kernel", "tma")
+    assert run() == d0
