@@ -221,7 +221,12 @@ def run_ours(args):
                 "step_kernel": args.kernel,
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": ncu_traffic(w, nb, Np),
+                         "algorithmic_bytes": step_bytes,
+                         "traffic_source": NCU_SUMMARY_NAME + " (dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum of one fused-step launch, "
+                                           "ncu --set full)",
                          "peak_source": peak_kind,
                          "note": "algorithmic bytes nnz*(16+4)+5*D*n_b*16 per fused step "
                                  "(SURVEY §8d) / (timed region / (steps*N_p) launches)"},
@@ -236,6 +241,23 @@ def run_ours(args):
         dist.destroy_process_group()
     ctx.close()
     return out
+
+
+NCU_SUMMARY_NAME = "profiles/r01_c2_fused_step.json"
+
+
+def ncu_traffic(w, nb, Np):
+    """DRAM bytes per fused-step launch from the committed ncu --set full
+    summary of this workload (None when the bench runs another shape)."""
+    path = os.path.join(ROOT, NCU_SUMMARY_NAME)
+    if (w["lx"], w["ly"], w["lz"], nb, Np) != (64, 64, 64, 32, 100) or not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            rec = json.load(f)["full"][0]
+        return float(rec["traffic_bytes"])
+    except (OSError, KeyError, ValueError, IndexError):
+        return None
 
 
 def e2e_steps_note(n):

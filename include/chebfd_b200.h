@@ -365,8 +365,9 @@ typedef struct {
     double total_spmvms, sigma, eta, bounds_lo, bounds_hi, matrix_norm_est, n_target_estimate;
     double seconds, weight_integral;
     /* wall seconds per phase: Lanczos bounds, KPM DOS, filter design, all
-     * apply_filter calls, SVQB (incl. rank repair), Rayleigh-Ritz */
-    double t_bounds, t_dos, t_design, t_filter, t_ortho, t_rr;
+     * apply_filter calls, SVQB (incl. rank repair), Rayleigh-Ritz, start block
+     * (randomize + normalise) */
+    double t_bounds, t_dos, t_design, t_filter, t_ortho, t_rr, t_start;
 } chebfd_solve_report;
 
 /* values/residual_norms/accepted: capacity `cap` >= n_search; history:

@@ -64,7 +64,7 @@ class chebfd_solve_report(C.Structure):
                 ("bounds_lo", _dbl), ("bounds_hi", _dbl), ("matrix_norm_est", _dbl),
                 ("n_target_estimate", _dbl), ("seconds", _dbl), ("weight_integral", _dbl),
                 ("t_bounds", _dbl), ("t_dos", _dbl), ("t_design", _dbl), ("t_filter", _dbl),
-                ("t_ortho", _dbl), ("t_rr", _dbl)]
+                ("t_ortho", _dbl), ("t_rr", _dbl), ("t_start", _dbl)]
 
 
 _SIGS = {

@@ -742,7 +742,7 @@ def solve(A: SparseMatrix, opts: SolverOptions) -> ConvergenceReport:
                              hist[:rep.iterations].copy(), rep.weight_integral,
                              bool(opts.collect_weight_density), rep.seconds,
                              {k: getattr(rep, "t_" + k) for k in
-                              ("bounds", "dos", "design", "filter", "ortho", "rr")})
+                              ("bounds", "dos", "design", "filter", "ortho", "rr", "start")})
 
 
 # ----------------------------------------------------- bench conventions --

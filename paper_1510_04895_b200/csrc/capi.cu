@@ -75,6 +75,54 @@ void* Context::pinned(size_t bytes) {
     return host_pinned;
 }
 
+// ---------------------------------------------------------- start blocks --
+// BlockVector::randomize (block_vector.hpp:42-51) of this rank's rows: the
+// reference's stream generated on the host (all threads) in pieces of one RNG
+// chunk per thread, into two pinned buffers, each piece's upload overlapping
+// the generation of the next.
+void randomize_upload(Context& c, Block& b, uint64_t seed) {
+    const int64_t count = b.rows * b.width;
+    const size_t esz = b.kind ? 16 : 8;
+    const int64_t first = b.row_begin * b.width;
+    const int64_t kPiece = std::max<int64_t>(
+        int64_t{1} << 22,
+        std::min<int64_t>(NormalStream::parallel_piece(b.kind), (int64_t{1} << 30) / esz));
+    if (count <= kPiece) {
+        std::vector<double> h(static_cast<size_t>(count) * (b.kind ? 2 : 1));
+        host_randomize(b.kind, seed, first, count, h.data());
+        if (count)
+            CFD_CUDA(cudaMemcpyAsync(b.owned(), h.data(), b.owned_bytes(), cudaMemcpyHostToDevice,
+                                     c.stream));
+        ctx_sync(c);
+        return;
+    }
+    char* pin = static_cast<char*>(c.pinned(2 * kPiece * esz));
+    cudaEvent_t done[2];
+    CFD_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    CFD_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    NormalStream ns(seed);
+    char* dev = static_cast<char*>(b.owned());
+    try {
+        for (int64_t off = 0, k = 0; off < count; off += kPiece, ++k) {
+            const int buf = static_cast<int>(k & 1);
+            const int64_t n = std::min(kPiece, count - off);
+            char* h = pin + buf * kPiece * esz;
+            if (k >= 2) CFD_CUDA(cudaEventSynchronize(done[buf]));
+            ns.emit(b.kind, first + off, n, h);
+            CFD_CUDA(cudaMemcpyAsync(dev + off * esz, h, n * esz, cudaMemcpyHostToDevice, c.stream));
+            CFD_CUDA(cudaEventRecord(done[buf], c.stream));
+        }
+        ctx_sync(c);
+    } catch (...) {
+        cudaStreamSynchronize(c.stream);
+        cudaEventDestroy(done[0]);
+        cudaEventDestroy(done[1]);
+        throw;
+    }
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+}
+
 // ---------------------------------------------------------------- helpers --
 void ctx_sync(Context& c) { CFD_CUDA(cudaStreamSynchronize(c.stream)); }
 
@@ -819,17 +867,7 @@ int chebfd_block_zero(chebfd_block* b) {
 }
 
 int chebfd_block_randomize(chebfd_block* b, uint64_t seed) {
-    return guard([&] {
-        Block* x = reinterpret_cast<Block*>(b);
-        Context& c = *x->ctx;
-        const int64_t count = x->rows * x->width;
-        std::vector<double> h(static_cast<size_t>(count) * (x->kind ? 2 : 1));
-        host_randomize(x->kind, seed, x->row_begin * x->width, count, h.data());
-        if (count)
-            CFD_CUDA(cudaMemcpyAsync(x->owned(), h.data(), x->owned_bytes(),
-                                     cudaMemcpyHostToDevice, c.stream));
-        ctx_sync(c);
-    });
+    return guard([&] { randomize_upload(*reinterpret_cast<Block*>(b)->ctx, *reinterpret_cast<Block*>(b), seed); });
 }
 
 int chebfd_block_randomize_device(chebfd_block* b, uint64_t seed) {

@@ -35,6 +35,8 @@ void ctx_sync(Context& c);
 std::unique_ptr<Block> make_block(Context& c, const Matrix* m, int kind, int64_t rows,
                                   int64_t width, bool zero = true);
 void check_same_shape(const Block& x, const Block& y);
+// BlockVector::randomize of this rank's rows, streamed host -> device
+void randomize_upload(Context& c, Block& b, uint64_t seed);
 void check_conforms(const Matrix& a, const Block& x, const char* who);
 void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered);
 void allreduce_sum(Context& c, double* dev, size_t n, cudaStream_t st);

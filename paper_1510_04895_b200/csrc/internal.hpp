@@ -247,6 +247,20 @@ void validate_lattice(const chebfd_lattice& s, bool needs_z);
 // std::mt19937_64 + std::normal_distribution stream (block_vector.hpp:42-51):
 // entries [first, first+count) of the row-major global block
 void host_randomize(int kind, uint64_t seed, int64_t first, int64_t count, void* out);
+// The same stream generated piecewise: emit() ranges in increasing order reuse
+// the chunk bookkeeping of earlier calls (jump-ahead + parallel polar method).
+class NormalStream {
+  public:
+    explicit NormalStream(uint64_t seed);
+    ~NormalStream();
+    void emit(int kind, int64_t first, int64_t count, void* out);
+    // entries per emit() call that keep every host thread busy
+    static int64_t parallel_piece(int kind);
+
+  private:
+    struct Impl;
+    std::unique_ptr<Impl> impl_;
+};
 std::vector<double> window_coeffs(double tlo, double thi, double blo, double bhi, int degree);
 std::vector<double> kernel_coeffs(int kind, int mu, int degree);
 double dos_count(const double* mu, int order, double blo, double bhi, double lo, double hi);

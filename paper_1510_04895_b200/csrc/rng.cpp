@@ -45,6 +45,25 @@ struct Window {
         i = i + 1 == kN ? 0 : i + 1;
         return w;
     }
+    // rotate so logical word 0 sits at x[0] (the layout std::mt19937_64 twists in place)
+    void normalize() {
+        if (i == 0) return;
+        uint64_t t[kN];
+        for (int j = 0; j < kN; ++j) t[j] = x[i + j >= kN ? i + j - kN : i + j];
+        std::memcpy(x, t, sizeof(x));
+        i = 0;
+    }
+    // the next 312 outputs at once (normalized window; == 312 next() calls)
+    void twist() {
+        auto mix = [](uint64_t a, uint64_t b, uint64_t c) {
+            const uint64_t y = (a & kUM) | (b & kLM);
+            return c ^ (y >> 1) ^ ((0ULL - (y & 1ULL)) & kA);  // branch-free
+        };
+        int k = 0;
+        for (; k < kN - kM; ++k) x[k] = mix(x[k], x[k + 1], x[k + kM]);
+        for (; k < kN - 1; ++k) x[k] = mix(x[k], x[k + 1], x[k + kM - kN]);
+        x[kN - 1] = mix(x[kN - 1], x[0], x[kM - 1]);
+    }
     void xor_in(const Window& o) {
         // logical word j: x[(i+j)%N] ^= o.x[(o.i+j)%N], in straight segments
         int j = 0;
@@ -191,17 +210,33 @@ const Poly& chunk_jump() {
 
 // libstdc++ generate_canonical<double, 53>(mt19937_64)
 inline double canon(uint64_t u) {
-    double r = static_cast<double>(u) / 18446744073709551616.0;
+    // / 2^64 == * 2^-64 exactly (power-of-two scaling; the only rounding is the conversion)
+    double r = static_cast<double>(u) * 0x1p-64;
     if (r >= 1.0) r = std::nextafter(1.0, 0.0);
     return r;
 }
 
+// the chunk's uniform words, 312 per twist (kN is even, so pairs never straddle)
+struct Words {
+    Window w;
+    int pos = kN;
+    explicit Words(const Window& start) : w(start) { w.normalize(); }
+    uint64_t next() {
+        if (pos == kN) {
+            w.twist();
+            pos = 0;
+        }
+        return w.x[pos++];
+    }
+};
+
 // count accepted polar pairs among the chunk's kChunkOut uniforms
-int64_t count_pairs(Window w) {
+int64_t count_pairs(const Window& start) {
+    Words src(start);
     int64_t acc = 0;
     for (uint64_t k = 0; k < kChunkOut; k += 2) {
-        const double x = 2.0 * canon(temper(w.next())) - 1.0;
-        const double y = 2.0 * canon(temper(w.next())) - 1.0;
+        const double x = 2.0 * canon(temper(src.next())) - 1.0;
+        const double y = 2.0 * canon(temper(src.next())) - 1.0;
         const double r2 = x * x + y * y;
         acc += !(r2 > 1.0 || r2 == 0.0);
     }
@@ -212,12 +247,13 @@ int64_t count_pairs(Window w) {
 // index).  Pair j of the stream is normals (2j, 2j+1) = (y m, x m).  Complex
 // entries are (re, im) = (normal 2i+1, normal 2i), i.e. pair j lands as
 // (x m, y m) at entry j - E0; real normals land at index n - n_begin.
-void emit_pairs(Window w, int64_t p0, int64_t p1, int64_t pbase, bool cplx, int64_t n_begin,
-                int64_t n_end, double* out) {
+void emit_pairs(const Window& start, int64_t p0, int64_t p1, int64_t pbase, bool cplx,
+                int64_t n_begin, int64_t n_end, double* out) {
+    Words src(start);
     int64_t pj = 0;
     for (uint64_t k = 0; k < kChunkOut && pj < p1; k += 2) {
-        const double x = 2.0 * canon(temper(w.next())) - 1.0;
-        const double y = 2.0 * canon(temper(w.next())) - 1.0;
+        const double x = 2.0 * canon(temper(src.next())) - 1.0;
+        const double y = 2.0 * canon(temper(src.next())) - 1.0;
         const double r2 = x * x + y * y;
         if (r2 > 1.0 || r2 == 0.0) continue;
         if (pj >= p0) {
@@ -258,58 +294,90 @@ void serial(int kind, uint64_t seed, int64_t first, int64_t count, double* o) {
 
 }  // namespace
 
-// Entries [first, first+count) of the row-major global block's stream.
-void host_randomize(int kind, uint64_t seed, int64_t first, int64_t count, void* out) {
-    double* o = static_cast<double*>(out);
-    const int per = kind == CHEBFD_COMPLEX128 ? 2 : 1;
-    const int64_t n_begin = first * per, n_end = (first + count) * per;  // normal indices
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    if (n_end < (int64_t{1} << 23) || hw == 1) return serial(kind, seed, first, count, o);
-    // pairs [P0, P1) hold normals [2 P0, 2 P1) covering [n_begin, n_end)
-    const int64_t P0 = n_begin / 2, P1 = (n_end + 1) / 2;
-    const Poly& g = chunk_jump();
-    std::vector<Window> starts{seed_window(seed)};
+// Chunk bookkeeping of one seed's stream, extended on demand so a block can be
+// generated piecewise in increasing order (pass 1 is never repeated).
+struct NormalStream::Impl {
+    std::vector<Window> starts;
     std::vector<int64_t> pairs;  // accepted pairs per chunk
+    std::vector<int64_t> base{0};
     int64_t total = 0;
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    explicit Impl(uint64_t seed) : starts{seed_window(seed)} {}
+
     // pass 1: chunk start windows (sequential jumps) and pair counts (parallel)
-    while (total < P1) {
-        const int64_t have = static_cast<int64_t>(pairs.size());
-        const double est = static_cast<double>(P1 - total) / (0.785 * (kChunkOut / 2));
-        const int64_t batch = std::max<int64_t>(static_cast<int64_t>(hw),
-                                                static_cast<int64_t>(std::ceil(est * 1.02)) + 1);
-        while (static_cast<int64_t>(starts.size()) < have + batch + 1) {
-            Window w = starts.back();
-            apply(g, w);
-            starts.push_back(w);
+    void count_to(int64_t P1) {
+        const Poly& g = chunk_jump();
+        while (total < P1) {
+            const int64_t have = static_cast<int64_t>(pairs.size());
+            const double est = static_cast<double>(P1 - total) / (0.785 * (kChunkOut / 2));
+            const int64_t batch = std::max<int64_t>(static_cast<int64_t>(hw),
+                                                    static_cast<int64_t>(std::ceil(est * 1.02)) + 1);
+            while (static_cast<int64_t>(starts.size()) < have + batch + 1) {
+                Window w = starts.back();
+                apply(g, w);
+                starts.push_back(w);
+            }
+            pairs.resize(have + batch);
+            std::vector<std::thread> th;
+            for (unsigned t = 0; t < hw; ++t)
+                th.emplace_back([&, t] {
+                    for (int64_t c = have + t; c < have + batch; c += hw)
+                        pairs[c] = count_pairs(starts[c]);
+                });
+            for (auto& x : th) x.join();
+            for (int64_t c = have; c < have + batch; ++c) {
+                total += pairs[c];
+                base.push_back(total);
+            }
         }
-        pairs.resize(have + batch);
+    }
+
+    // pass 2: emit the normals of pairs [P0, P1) straight into `o` (chunks in parallel)
+    void emit(int kind, int64_t first, int64_t count, double* o) {
+        const int per = kind == CHEBFD_COMPLEX128 ? 2 : 1;
+        const int64_t n_begin = first * per, n_end = (first + count) * per;  // normal indices
+        // pairs [P0, P1) hold normals [2 P0, 2 P1) covering [n_begin, n_end)
+        const int64_t P0 = n_begin / 2, P1 = (n_end + 1) / 2;
+        count_to(P1);
+        std::vector<int64_t> todo;
+        for (size_t c = 0; c < pairs.size(); ++c)
+            if (base[c + 1] > P0 && base[c] < P1) todo.push_back(static_cast<int64_t>(c));
+        const bool cplx = kind == CHEBFD_COMPLEX128;
         std::vector<std::thread> th;
         for (unsigned t = 0; t < hw; ++t)
             th.emplace_back([&, t] {
-                for (int64_t c = have + t; c < have + batch; c += hw) pairs[c] = count_pairs(starts[c]);
+                for (size_t q = t; q < todo.size(); q += hw) {
+                    const int64_t c = todo[q];
+                    const int64_t lo = std::max(P0, base[c]) - base[c];
+                    const int64_t hi = std::min(P1, base[c + 1]) - base[c];
+                    emit_pairs(starts[c], lo, hi, base[c], cplx, n_begin, n_end, o);
+                }
             });
         for (auto& x : th) x.join();
-        total = 0;
-        for (int64_t v : pairs) total += v;
     }
-    // pass 2: emit the normals of pairs [P0, P1) straight into `o` (chunks in parallel)
-    std::vector<int64_t> base(pairs.size() + 1, 0);
-    for (size_t c = 0; c < pairs.size(); ++c) base[c + 1] = base[c] + pairs[c];
-    std::vector<int64_t> todo;
-    for (size_t c = 0; c < pairs.size(); ++c)
-        if (base[c + 1] > P0 && base[c] < P1) todo.push_back(static_cast<int64_t>(c));
-    const bool cplx = kind == CHEBFD_COMPLEX128;
-    std::vector<std::thread> th;
-    for (unsigned t = 0; t < hw; ++t)
-        th.emplace_back([&, t] {
-            for (size_t q = t; q < todo.size(); q += hw) {
-                const int64_t c = todo[q];
-                const int64_t lo = std::max(P0, base[c]) - base[c];
-                const int64_t hi = std::min(P1, base[c + 1]) - base[c];
-                emit_pairs(starts[c], lo, hi, base[c], cplx, n_begin, n_end, o);
-            }
-        });
-    for (auto& x : th) x.join();
+};
+
+int64_t NormalStream::parallel_piece(int kind) {
+    // one RNG chunk per host thread: ~0.785 accepted pairs per uniform pair
+    const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t normals = hw * static_cast<int64_t>(0.785 * kChunkOut);
+    return normals / (kind == CHEBFD_COMPLEX128 ? 2 : 1);
+}
+
+NormalStream::NormalStream(uint64_t seed) : impl_(std::make_unique<Impl>(seed)) {}
+NormalStream::~NormalStream() = default;
+void NormalStream::emit(int kind, int64_t first, int64_t count, void* out) {
+    impl_->emit(kind, first, count, static_cast<double*>(out));
+}
+
+// Entries [first, first+count) of the row-major global block's stream.
+void host_randomize(int kind, uint64_t seed, int64_t first, int64_t count, void* out) {
+    const int per = kind == CHEBFD_COMPLEX128 ? 2 : 1;
+    const int64_t n_end = (first + count) * per;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    if (n_end < (int64_t{1} << 23) || hw == 1)
+        return serial(kind, seed, first, count, static_cast<double*>(out));
+    NormalStream(seed).emit(kind, first, count, out);
 }
 
 }  // namespace cfd

@@ -149,15 +149,7 @@ std::vector<double> norms(Context& c, const Block& x) {
     return n;
 }
 
-void randomize(Context& c, Block& b, uint64_t seed) {
-    const int64_t count = b.rows * b.width;
-    std::vector<double> h(static_cast<size_t>(count) * (b.kind ? 2 : 1));
-    host_randomize(b.kind, seed, b.row_begin * b.width, count, h.data());
-    if (count)
-        CFD_CUDA(cudaMemcpyAsync(b.owned(), h.data(), b.owned_bytes(), cudaMemcpyHostToDevice,
-                                 c.stream));
-    ctx_sync(c);
-}
+void randomize(Context& c, Block& b, uint64_t seed) { randomize_upload(c, b, seed); }
 
 // symmetric tridiagonal eigenvalues (Lanczos T) via cuSOLVER
 std::vector<double> tridiag_eigs(Context& c, const std::vector<double>& al,
@@ -450,9 +442,11 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
         const double required =
             std::max(1.0, std::ceil(rep->n_target_estimate - 3.0 * std::sqrt(rep->n_target_estimate)));
         const int64_t ns = rep->n_search;
+        tp = clk::now();
         auto x = make_block(c, &A, A.kind, A.part.local, ns, false);
         randomize(c, *x, o->seed + 2);
         divide_columns(c, *x, norms(c, *x));  // unit columns (solver.cpp:149-154)
+        rep->t_start = secs(tp);
         Ritz ritz;
         std::vector<double> mom;
         for (int iter = 1; iter <= o->max_iters; ++iter) {

@@ -264,3 +264,18 @@ def test_set_option_invalidates_captured_filters(ctx, orc):
         ctx.set_option("slab_units", 0)
         ctx.set_option("kernel", "tma")
     assert run() == d0
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_streamed_randomize_matches_reference_stream(ctx, cplx):
+    """Blocks above 4 M entries are randomized in pieces through pinned
+    buffers (NormalStream); every piece continues the reference's stream."""
+    if cplx:
+        A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(16, 16, 64, disorder=0.5))
+        nb = 81  # 65536 x 81 = 5.3 M entries: two pieces
+    else:
+        A = cf.SparseMatrix.graphene(ctx, cf.LatticeSpec(512, 256, disorder=0.5))
+        nb = 19  # 262144 x 19 = 4.98 M entries: one full piece + a ragged tail
+    X = cf.BlockVector(A, nb).randomize(11)
+    want = cf.host_randomize(A.dim(), nb, 11, cplx)
+    assert bits_equal(X.to_numpy(), want)

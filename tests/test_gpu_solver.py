@@ -209,4 +209,4 @@ def test_solve_automatic_degree_matches_reference(ctx):
     assert abs(rep.sigma - g["sigma"]) <= 1e-9 * g["sigma"]
     acc = np.sort(rep.ritz.values[rep.ritz.accepted])
     assert np.max(np.abs(acc - np.array(g["accepted_values"]))) <= 1e-10
-    assert set(rep.timings) == {"bounds", "dos", "design", "filter", "ortho", "rr"}
+    assert set(rep.timings) == {"bounds", "dos", "design", "filter", "ortho", "rr", "start"}
