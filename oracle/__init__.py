@@ -361,6 +361,8 @@ class Ref:
         L.ref_block_save.argtypes = [C.c_int, _i64, _i64, _vp, C.c_char_p]
         L.ref_block_load.argtypes = [C.c_int, C.c_char_p, _vp, _vp, _vp]
         L.ref_bench_filter.argtypes = [_vp, _vp, C.c_int, C.c_int, _dbl, _vp]
+        L.ref_damping_factor.argtypes = [_dbl, _dbl, _dbl, _dbl, _dbl, C.c_int, C.c_int, C.c_int,
+                                         _vp]
         if threads is not None:
             L.ref_set_threads(threads)
 
@@ -582,6 +584,13 @@ class Ref:
         out = np.zeros((len(sz), 8))
         self._chk(self.lib.ref_bench_filter(m.h, _ptr(sz), len(sz), degree, bandwidth, _ptr(out)))
         return out
+
+    def damping_factor(self, target, delta_prime, bounds, degree, kernel="lanczos2"):
+        k, kmu = _kernel_code(kernel)
+        out = _dbl()
+        self._chk(self.lib.ref_damping_factor(target[0], target[1], delta_prime, bounds[0],
+                                              bounds[1], degree, k, kmu, C.byref(out)))
+        return out.value
 
 
 def ref_available():

@@ -627,4 +627,17 @@ int ref_bench_filter(void* h, const int* sizes, int n, int degree, double bandwi
     });
 }
 
+// damping_factor (filter_design.cpp:178-184) of make_filter(target, bounds, degree, kernel)
+int ref_damping_factor(double tlo, double thi, double dprime, double blo, double bhi, int degree,
+                       int kind, int mu, double* out) {
+    return guard([&] {
+        const FilterPolynomial p = make_filter({tlo, thi}, {blo, bhi}, degree, kernel_of(kind, mu));
+        IntervalConfig cfg;
+        cfg.target = {tlo, thi};
+        cfg.delta_prime = dprime;
+        cfg.bounds = {blo, bhi};
+        *out = damping_factor(p, cfg);
+    });
+}
+
 }  // extern "C"

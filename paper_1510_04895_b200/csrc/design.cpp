@@ -8,6 +8,7 @@
 #include <cmath>
 #include <limits>
 #include <numbers>
+#include <thread>
 #include <vector>
 
 #include "capi_common.hpp"
@@ -57,6 +58,42 @@ Poly build(double tlo, double thi, double blo, double bhi, int degree, int kind,
     return p;
 }
 
+// First index of the extremum of f(j) over j = 0..n (skipping points where
+// f returns a negative value), exactly the serial scan's answer: threads scan
+// contiguous index ranges, and the merge keeps the smaller index on ties.
+// Parallel once n x degree is large (paper-scale degrees).
+template <class F>
+std::pair<long, double> arg_extremum(long n, int degree, bool maximize, const F& f) {
+    auto scan = [&](long j0, long j1) {
+        long bj = -1;
+        double bf = 0.0;
+        for (long j = j0; j < j1; ++j) {
+            const double v = f(j);
+            if (v < 0.0) continue;
+            if (bj < 0 || (maximize ? v > bf : v < bf)) {
+                bf = v;
+                bj = j;
+            }
+        }
+        return std::make_pair(bj, bf);
+    };
+    const long total = n + 1;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    if (hw == 1 || static_cast<double>(total) * degree < 4e6) return scan(0, total);
+    const long parts = std::min<long>(hw, total);
+    std::vector<std::pair<long, double>> res(static_cast<size_t>(parts));
+    std::vector<std::thread> th;
+    for (long q = 0; q < parts; ++q)
+        th.emplace_back([&, q] { res[q] = scan(total * q / parts, total * (q + 1) / parts); });
+    for (auto& t : th) t.join();
+    std::pair<long, double> best{-1, 0.0};
+    for (const auto& r : res) {  // ranges in increasing index order: strict comparison keeps the first
+        if (r.first < 0) continue;
+        if (best.first < 0 || (maximize ? r.second > best.second : r.second < best.second)) best = r;
+    }
+    return best;
+}
+
 // golden-section search for an extremum of |p| over theta in [lo, hi]
 double golden(const Poly& p, double lo, double hi, bool maximize) {
     const double r = (std::sqrt(5.0) - 1.0) / 2.0;
@@ -86,15 +123,8 @@ double golden(const Poly& p, double lo, double hi, bool maximize) {
 double scan_max(const Poly& p, double lo, double hi, long n) {
     if (!(hi > lo)) return p.mag(lo);
     const double step = (hi - lo) / static_cast<double>(n);
-    long best = 0;
-    double fb = -1.0;
-    for (long j = 0; j <= n; ++j) {
-        const double f = p.mag(lo + step * j);
-        if (f > fb) {
-            fb = f;
-            best = j;
-        }
-    }
+    const long best =
+        arg_extremum(n, p.degree, true, [&](long j) { return p.mag(lo + step * j); }).first;
     return golden(p, std::max(lo, lo + step * (best - 1)), std::min(hi, lo + step * (best + 1)), true);
 }
 
@@ -120,18 +150,12 @@ double sigma_of(const Poly& p, const Cfg& cfg) {
     // coarse grid in theta, points inside the search interval skipped
     const long m = std::max<long>(10L * p.degree, 2000);
     const double h = kPi / static_cast<double>(m);
-    long best_j = -1;
-    double best_th = 0.0, best_f = -1.0;
-    for (long j = 0; j <= m; ++j) {
-        const double th = h * j;
-        if (th > th_s_hi && th < th_s_lo) continue;
-        const double f = std::abs(p.at(p.x_at(th)));
-        if (best_j < 0 || f > best_f) {
-            best_f = f;
-            best_th = th;
-            best_j = j;
-        }
-    }
+    const long best_j = arg_extremum(m, p.degree, true, [&](long j) {
+                            const double th = h * j;
+                            if (th > th_s_hi && th < th_s_lo) return -1.0;  // inside I_S: skipped
+                            return std::abs(p.at(p.x_at(th)));
+                        }).first;
+    const double best_th = best_j >= 0 ? h * best_j : 0.0;
     double lo = best_th - h, hi = best_th + h;
     if (best_th <= th_s_hi) {
         lo = std::max(lo, 0.0);
@@ -148,15 +172,9 @@ double sigma_of(const Poly& p, const Cfg& cfg) {
     // minimum over the target interval
     const double span = th_t_lo - th_t_hi;
     const long mt = std::max<long>(200, static_cast<long>(10.0 * p.degree * span / kPi) + 1);
-    size_t bmin = 0;
-    double fmin = 0.0;
-    for (long j = 0; j <= mt; ++j) {
-        const double f = std::abs(p.at(p.x_at(th_t_hi + span * j / mt)));
-        if (j == 0 || f < fmin) {
-            fmin = f;
-            bmin = static_cast<size_t>(j);
-        }
-    }
+    const long bmin = arg_extremum(mt, p.degree, false, [&](long j) {
+                          return std::abs(p.at(p.x_at(th_t_hi + span * j / mt)));
+                      }).first;
     const double ht = span / mt;
     const double a = std::max(th_t_hi, th_t_hi + ht * (static_cast<double>(bmin) - 1));
     const double b = std::min(th_t_lo, th_t_hi + ht * (static_cast<double>(bmin) + 1));

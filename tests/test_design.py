@@ -61,6 +61,18 @@ def test_flat_dos_table_rows(ref):
     assert abs(d.eta_opt - 1023) <= 0.02 * 1023
     r = ref.choose_parameters(mu, (-1.0, 1.0), (-2.5e-3, 2.5e-3), 200, "lanczos2", 1e-12)
     assert d.np_opt == r["np_opt"]
+    # N_p ~ 2500: the sigma scans run threaded (arg-extremum merge keeps the
+    # serial first-index rule), so every bit still matches the serial reference
+    assert d.sigma == r["sigma"] and d.eta_opt == r["eta"] and d.delta_prime == r["delta_prime"]
+
+
+def test_parallel_scans_match_serial_reference_at_large_degree(ref):
+    """damping factors at paper-scale degrees (threaded scans)
+    equal the reference's serial ones bit for bit."""
+    for deg in (3000, 12000):
+        got = cf.damping_factor(cf.make_filter((-1e-3, 1e-3), (-1.0, 1.0), deg, "lanczos2"), 4e-3)
+        want = ref.damping_factor((-1e-3, 1e-3), 4e-3, (-1.0, 1.0), deg, "lanczos2")
+        assert got == want, deg
 
 
 def test_design_errors():
