@@ -299,6 +299,10 @@ typedef struct {
     double roofline;   /* P* = I(n_b) * b, Gflop/s */
     double efficiency; /* gflops / roofline */
 } chebfd_bench_point;
+/* intensity_model (bench.cpp:37-41): I(n_b) flop/byte of one blocked step.
+ * Errors (invalid_argument): n_b < 1, n_nzr <= 0. */
+int chebfd_intensity_model(double n_nzr, int s_d, int s_i, int f_a, int f_m, int n_b,
+                           double* out);
 /* bandwidth_probe_min_bytes (bench.cpp:42): 8 x the last-level cache (the GPU's L2). */
 int chebfd_bandwidth_probe_min_bytes(chebfd_ctx* ctx, uint64_t* out);
 /* bandwidth_probe (bench.cpp:44-67) on HBM: read-only streaming reduction over

@@ -107,6 +107,7 @@ _SIGS = {
     "chebfd_block_scale_columns": (_int, [_vp, _vp]),
     "chebfd_block_copy_columns": (_int, [_vp, _i64, _vp, _i64, _i64]),
     "chebfd_block_device_ptr": (_int, [_vp, _pp]),
+    "chebfd_intensity_model": (_int, [_dbl, _int, _int, _int, _int, _int, C.POINTER(_dbl)]),
     "chebfd_bandwidth_probe_min_bytes": (_int, [_vp, C.POINTER(_u64)]),
     "chebfd_bandwidth_probe": (_int, [_vp, _u64, _int, C.POINTER(_dbl)]),
     "chebfd_bench_filter": (_int, [_vp, _vp, _int, _int, _dbl, _vp, C.POINTER(_dbl)]),

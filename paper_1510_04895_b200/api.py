@@ -757,12 +757,11 @@ def per_row_bytes(n_nzr, s_d, s_i, n_b):
 
 
 def intensity_model(n_nzr, s_d, s_i, f_a, f_m, n_b):
-    """bench.cpp:38-42"""
-    if n_b < 1:
-        raise InvalidArgument("intensity_model: block size must be >= 1")
-    if not n_nzr > 0:
-        raise InvalidArgument("intensity_model: N_nzr must be positive")
-    return per_row_flops(n_nzr, f_a, f_m) / per_row_bytes(n_nzr, s_d, s_i, n_b)
+    """intensity_model (bench.cpp:37-41) through the C ABI."""
+    out = C.c_double()
+    _check(_lib().chebfd_intensity_model(float(n_nzr), int(s_d), int(s_i), int(f_a), int(f_m),
+                                         int(n_b), C.byref(out)))
+    return out.value
 
 
 # ------------------------------------------------- distributed planning --

@@ -138,6 +138,17 @@ using namespace cfd;
 
 extern "C" {
 
+// intensity_model (bench.cpp:37-41)
+int chebfd_intensity_model(double n_nzr, int s_d, int s_i, int f_a, int f_m, int n_b, double* out) {
+    return guard([&] {
+        if (n_b < 1) fail(CHEBFD_ERR_INVALID_ARGUMENT, "intensity_model: block size must be >= 1");
+        if (!(n_nzr > 0.0))
+            fail(CHEBFD_ERR_INVALID_ARGUMENT, "intensity_model: N_nzr must be positive");
+        const Params p{n_nzr, s_d, s_i, f_a, f_m};
+        *out = per_row_flops(p) / per_row_bytes(p, n_b);
+    });
+}
+
 int chebfd_bandwidth_probe_min_bytes(chebfd_ctx* ctx, uint64_t* out) {
     return guard([&] { *out = probe_min_bytes(*reinterpret_cast<Context*>(ctx)); });
 }
