@@ -164,6 +164,7 @@ typedef struct {
     int64_t halo_lo, halo_hi; /* halo rows received from the lower / upper neighbour */
     int chunk;            /* SELL chunk height C */
     int max_row_len;
+    int stage_rows;       /* largest per-chunk gathered-row union of the staged plan (0: none) */
 } chebfd_matrix_info;
 int chebfd_matrix_get_info(const chebfd_matrix* a, chebfd_matrix_info* out);
 

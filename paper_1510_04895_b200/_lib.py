@@ -37,7 +37,8 @@ class chebfd_partition(C.Structure):
 class chebfd_matrix_info(C.Structure):
     _fields_ = [("kind", _int), ("dim", _i64), ("nnz", _i64), ("local_rows", _i64),
                 ("row_begin", _i64), ("local_nnz", _i64), ("sell_entries", _i64),
-                ("halo_lo", _i64), ("halo_hi", _i64), ("chunk", _int), ("max_row_len", _int)]
+                ("halo_lo", _i64), ("halo_hi", _i64), ("chunk", _int), ("max_row_len", _int),
+                ("stage_rows", _int)]
 
 
 class chebfd_design(C.Structure):

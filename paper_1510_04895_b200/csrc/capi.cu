@@ -231,7 +231,7 @@ void allreduce_sum(Context& c, double* dev, size_t n, cudaStream_t st) {
 // One Chebyshev-type step over all owned rows, with the halo exchange of the
 // gathered operand overlapped with the interior rows when distributed.
 void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
-    if (c.kernel_variant == 1 && s.alpha != 1.0) {
+    if (c.kernel_variant >= 1 && s.alpha != 1.0) {
         // the TMA step kernel reads values pre-multiplied by alpha; build the
         // copy now unless a graph is being captured (apply_filter pre-builds)
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -443,7 +443,7 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
     const int64_t nb = x.width;
     FilterWorkspace& ws = filter_workspace(c, a, nb, moments);
     Matrix& am = const_cast<Matrix&>(a);
-    if (c.kernel_variant == 1) {  // pre-scaled values for the start step (alpha) and 2 alpha steps
+    if (c.kernel_variant >= 1) {  // pre-scaled values for the start step (alpha) and 2 alpha steps
         ensure_scaled_values(c, am, alpha, c.stream);
         ensure_scaled_values(c, am, 2.0 * alpha, c.stream);
         if (am.scaled_evicted) {
@@ -785,6 +785,7 @@ int chebfd_matrix_get_info(const chebfd_matrix* a, chebfd_matrix_info* out) {
         out->halo_hi = m->part.halo_hi;
         out->chunk = kChunk;
         out->max_row_len = m->max_row_len;
+        out->stage_rows = m->stage_max_rows;
     });
 }
 

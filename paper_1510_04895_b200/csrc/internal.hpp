@@ -88,6 +88,8 @@ struct Context;
 
 // ---- SELL-C-sigma matrix (C = 32, sigma = 1) ---------------------------------------
 constexpr int kChunk = 32;
+constexpr int kStageRuns = 64;  // row runs per chunk in a staged-gather plan
+constexpr int kStageGap = 3;    // runs closer than this many rows are merged (copied together)
 
 struct Matrix {
     Context* ctx = nullptr;
@@ -101,6 +103,14 @@ struct Matrix {
     int64_t entries = 0;     // SELL slots (padding included)
     DeviceBuffer chunk_ptr;  // int64[nchunks+1], slot offsets
     DeviceBuffer chunk_full; // uint8[nchunks]: every row has exactly the chunk width
+    // staged-gather plan (kernel variant 2), per 32-row chunk: the rows of the
+    // gathered operand the chunk reads, as merged runs copied by TMA into
+    // shared memory, and each slot's / own row's index inside that copy
+    DeviceBuffer stage_runs;  // int4[nchunks * kStageRuns]: (first ext row, rows, local offset, 0)
+    DeviceBuffer stage_meta;  // int2[nchunks]: (runs, rows)
+    DeviceBuffer stage_lcol;  // uint16[nchunks * 32 * 16]: row-major within the chunk, 0xFFFF = padding
+    DeviceBuffer stage_lown;  // uint16[nchunks * 32]
+    int stage_max_rows = 0;   // largest per-chunk row union (0: no plan)
     DeviceBuffer cols;       // int32[entries], extended-row index or -1 padding
     DeviceBuffer vals;       // double or double2 [entries]
     // value copies pre-multiplied by a step's alpha (apply_filter uses alpha
@@ -165,7 +175,8 @@ struct Context {
     cusolverDnContext* cusolver = nullptr;
     ncclComm_t nccl = nullptr;
     bool use_graphs = true, overlap = true;
-    int kernel_variant = 1;  // step kernel: 0 register gathers, 1 TMA-staged matrix chunks
+    int kernel_variant = 1;  // step kernel: 0 register gathers, 1 TMA-staged matrix chunks,
+                             // 2 TMA-staged matrix chunks + gathered rows (where a plan fits)
     int64_t launches = 0;
     int slab_units = 0;   // step kernel column-slab width in 16-byte units (0: up to 256)
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)

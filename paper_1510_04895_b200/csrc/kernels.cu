@@ -591,6 +591,217 @@ __global__ void __launch_bounds__(256, CFD_TMA_MINB) step_tma_kernel(const StepP
     }
 }
 
+// ---- staged-gather step kernel (kernel variant 2) -------------------------------------------
+// One tile = one 32-row SELL chunk, one CTA per SM, two shared-memory stages.
+// Warp 0 stages tile k+1 by TMA bulk copies -- the chunk's values, its plan
+// (16-bit local column indices, row-major per row) and every run of gathered
+// rows the chunk reads -- while the CTA computes tile k entirely from shared
+// memory; W / X (/ x0) of tile k+1 are prefetched into registers.  No gather
+// is in flight in registers, so the latency that bounds the TMA kernel's
+// 16 warps/SM is replaced by bulk copies.  One warp = one row slot (32 units
+// = 512 B: complex n_b = 32 or real n_b = 64); 8 warps x 4 rows per tile.
+// Accumulation order per row = stored order: bit-identical to step_tma_kernel.
+struct StagePlan {
+    const int4* runs;
+    const int2* meta;
+    const unsigned short* lcol;
+    const unsigned short* lown;
+    int cap_rows;  // U rows per stage
+    int nstage;    // shared-memory stages (2 or 3): tiles staged ahead = nstage - 1
+};
+
+template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
+__global__ void __launch_bounds__(256, 1) step_stage_kernel(const StepParams p, const StagePlan sp) {
+    using O = Ops<CPLX, T>;
+    using M = typename O::M;
+    constexpr int US = 32, R = 8, NP = 4;
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
+    constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
+    constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[3];
+    const int t = threadIdx.x;
+    const int rr = t >> 5, u = t & 31;
+    const int ns = sp.nstage;
+    const size_t u_bytes = static_cast<size_t>(sp.cap_rows) * US * sizeof(T);
+    const size_t v_bytes = 32 * MAXW * sizeof(M);
+    const size_t stage_bytes = u_bytes + v_bytes + 32 * 16 * 2 + 32 * 2;
+    auto U_s = [&](int b) { return reinterpret_cast<const T*>(smem_raw + b * stage_bytes); };
+    auto V_s = [&](int b) { return reinterpret_cast<const M*>(smem_raw + b * stage_bytes + u_bytes); };
+    auto LC_s = [&](int b) {
+        return reinterpret_cast<const unsigned short*>(smem_raw + b * stage_bytes + u_bytes + v_bytes);
+    };
+    auto LO_s = [&](int b) {
+        return reinterpret_cast<const unsigned short*>(smem_raw + b * stage_bytes + u_bytes + v_bytes +
+                                                       1024);
+    };
+
+    const T* __restrict__ in = static_cast<const T*>(p.in);
+    T* __restrict__ W = static_cast<T*>(p.w) + u;
+    T* __restrict__ X = static_cast<T*>(p.x) + u;
+    T* __restrict__ X0 = static_cast<T*>(p.x0) + u;
+    const M* __restrict__ gvals = static_cast<const M*>(p.svals);
+    const int pitch = p.pitch;
+    double coeff = p.c0, c1 = p.c1, c2 = p.c2;
+    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepStart2 && p.coeff_dev) {
+        coeff = p.coeff_dev[0];
+        c1 = p.coeff_dev[1];
+        c2 = p.coeff_dev[2];
+    }
+    T acc_d[NDOT > 0 ? NDOT : 1];
+    T comp_d[NDOT > 0 ? NDOT : 1];
+#pragma unroll
+    for (int d = 0; d < (NDOT > 0 ? NDOT : 1); ++d) {
+        acc_d[d] = O::zero();
+        comp_d[d] = O::zero();
+    }
+    const int64_t row0 = p.row0, row1 = p.row1;
+    const int64_t cbeg = row0 >> 5;
+    const int64_t ntiles = row1 > row0 ? ((row1 + 31) >> 5) - cbeg : 0;
+    const int64_t* __restrict__ cptr = p.chunk_ptr;
+
+    // warp 0 stages chunk c into buffer b
+    auto issue = [&](int64_t tile, int b) {
+        const int64_t c = cbeg + tile;
+        const int2 meta = sp.meta[c];
+        const int64_t s0 = cptr[c];
+        const unsigned nslot = static_cast<unsigned>(cptr[c + 1] - s0);
+        unsigned char* base = smem_raw + b * stage_bytes;
+        if (u == 0) {
+            const unsigned total = static_cast<unsigned>(meta.y) * US * sizeof(T) +
+                                   nslot * static_cast<unsigned>(sizeof(M)) + 1024 + 64;
+            mbar_arrive_expect_tx(&bars[b], total);
+            if (nslot) tma_load_1d(base + u_bytes, gvals + s0, nslot * sizeof(M), &bars[b]);
+            tma_load_1d(base + u_bytes + v_bytes, sp.lcol + c * 512, 1024, &bars[b]);
+            tma_load_1d(base + u_bytes + v_bytes + 1024, sp.lown + c * 32, 64, &bars[b]);
+        }
+        __syncwarp();
+        for (int k = u; k < meta.x; k += 32) {
+            const int4 run = sp.runs[c * kStageRuns + k];
+            tma_load_1d(base + static_cast<size_t>(run.z) * US * sizeof(T),
+                        in + static_cast<int64_t>(run.x) * pitch,
+                        static_cast<unsigned>(run.y) * US * sizeof(T), &bars[b]);
+        }
+    };
+
+    T wn[NP], xn[NP], x0n[NP];
+    int64_t s0n = 0, s1n = 0;
+    int fulln = 0;
+    auto prefetch_rows = [&](int64_t tile) {
+        const int64_t c = cbeg + tile;
+        s0n = __ldg(&cptr[c]);
+        s1n = __ldg(&cptr[c + 1]);
+        fulln = __ldg(&p.chunk_full[c]);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            const int64_t r = c * 32 + rr + i * R;
+            if (r >= row0 && r < row1) {
+                if constexpr (HAS_W) wn[i] = ld_stream(&W[r * pitch]);
+                if constexpr (HAS_X) xn[i] = ld_stream(&X[r * pitch]);
+                if constexpr (HAS_X0) x0n[i] = ld_stream(&X0[r * pitch]);
+            }
+        }
+    };
+
+    if (t == 0) {
+        for (int b = 0; b < ns; ++b) mbar_init(&bars[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    int64_t tile = blockIdx.x;
+    // prologue: stage the first ns - 1 tiles
+    for (int b = 0; b + 1 < ns; ++b)
+        if (rr == 0 && tile + b * static_cast<int64_t>(gridDim.x) < ntiles)
+            issue(tile + b * static_cast<int64_t>(gridDim.x), b);
+    if (tile < ntiles) prefetch_rows(tile);
+    unsigned phases = 0u;
+    for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+        const int buf = k % ns;
+        const bool more = tile + gridDim.x < ntiles;
+        // refill the stage tile k - 1 used (every thread passed the barrier ending k - 1)
+        const int64_t ahead = tile + static_cast<int64_t>(ns - 1) * gridDim.x;
+        if (rr == 0 && ahead < ntiles) issue(ahead, (k + ns - 1) % ns);
+        T wc[NP], xc[NP], x0c[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            wc[i] = wn[i];
+            xc[i] = xn[i];
+            x0c[i] = x0n[i];
+        }
+        const int64_t c = cbeg + tile;
+        const int64_t s0 = s0n;
+        const int w = static_cast<int>((s1n - s0) >> 5);
+        const bool fast = w == MAXW && fulln != 0 && c * 32 >= row0 && c * 32 + 32 <= row1;
+        if (more) prefetch_rows(tile + gridDim.x);
+        mbar_wait(&bars[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        const T* us = U_s(buf);
+        const M* vs = V_s(buf);
+        const unsigned short* lcs = LC_s(buf);
+        const unsigned short* los = LO_s(buf);
+        // the warp's NP rows advance together: NP independent accumulation chains
+        unsigned qw[NP][8];
+        bool act[NP];
+        T acc[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            const int l = rr + i * R;
+            const int64_t r = c * 32 + l;
+            act[i] = fast || (r >= row0 && r < row1);
+            const uint4 q0 = *reinterpret_cast<const uint4*>(lcs + l * 16);  // broadcast
+            const uint4 q1 = *reinterpret_cast<const uint4*>(lcs + l * 16 + 8);
+            qw[i][0] = q0.x; qw[i][1] = q0.y; qw[i][2] = q0.z; qw[i][3] = q0.w;
+            qw[i][4] = q1.x; qw[i][5] = q1.y; qw[i][6] = q1.z; qw[i][7] = q1.w;
+            acc[i] = O::zero();
+        }
+        if (fast) {
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j)
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                    const unsigned lc = (qw[i][j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+                    acc[i] = O::vadd(acc[i], O::prod(vs[j * 32 + rr + i * R], us[lc * US + u]));
+                }
+        } else {
+#pragma unroll
+            for (int j = 0; j < MAXW; ++j)
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                    const unsigned lc = (qw[i][j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+                    if (act[i] && j < w && lc != 0xFFFFu)
+                        acc[i] = O::vadd(acc[i], O::prod(vs[j * 32 + rr + i * R], us[lc * US + u]));
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            if (!act[i]) continue;
+            const int l = rr + i * R;
+            const T ui = us[static_cast<int>(los[l]) * US + u];
+            step_epilogue<O, T, KIND, DMODE>(acc[i], ui, wc[i], xc[i], x0c[i], (c * 32 + l) * pitch,
+                                             W, X, X0, p.beta, coeff, c1, c2, acc_d, comp_d);
+        }
+        __syncthreads();  // stage `buf` is refilled by the next iteration's issue
+    }
+
+    if constexpr (NDOT > 0) {
+        T acc_out[NDOT];
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) acc_out[d] = acc_d[d];
+        void* outp = p.dots_out;
+        const int64_t dstride = p.dots_row_stride;
+        grid_reduce<T, NDOT>(acc_out, R, US, static_cast<T*>(p.partials), p.part_base + blockIdx.x,
+                             p.nparts, p.final_launch != 0, p.counter,
+                             [&](int d, int uu, T vv) {
+                                 if (DMODE == 1)
+                                     O::store_full(static_cast<T*>(outp), uu, vv);
+                                 else
+                                     O::store_re(static_cast<double*>(outp) + d * dstride, uu, vv);
+                             });
+    }
+}
+
 // values pre-multiplied by s (one rounding per entry, as kernels.hpp:95)
 __global__ void scale_values_kernel(double* __restrict__ out, const double* __restrict__ in,
                                     int64_t n, double s) {
@@ -713,6 +924,107 @@ __global__ void sell_width_kernel(const int64_t* __restrict__ offs, int64_t rows
     atomicMax(maxlen, static_cast<int>(w));
 }
 
+// Staged-gather plan of one chunk per CTA: sort the extended rows the chunk
+// reads (its slots' columns and its own rows), merge them into runs (gaps of
+// < kStageGap rows are copied too), and map every slot / own row to its row in
+// the concatenated runs.  Overflowing chunks (> kStageRuns runs) flag the
+// matrix as unplannable.
+__global__ void __launch_bounds__(256) stage_plan_kernel(
+    const int64_t* __restrict__ chunk_ptr, const int* __restrict__ cols, int64_t rows,
+    int64_t halo_lo, int4* __restrict__ runs_out, int2* __restrict__ meta,
+    unsigned short* __restrict__ lcol, unsigned short* __restrict__ lown, int* __restrict__ max_rows,
+    int* __restrict__ overflow) {
+    __shared__ int v[1024];
+    __shared__ int4 runs[kStageRuns];
+    __shared__ int nruns_s, nrows_s, bad_s;
+    const int64_t c = blockIdx.x;
+    const int t = threadIdx.x;
+    const int64_t base = chunk_ptr[c];
+    const int w = static_cast<int>((chunk_ptr[c + 1] - base) >> 5);
+    for (int i = t; i < 1024; i += 256) v[i] = INT_MAX;
+    __syncthreads();
+    for (int s = t; s < 32 * w && s < 512; s += 256) {
+        const int col = cols[base + s];
+        v[s] = col >= 0 ? col : INT_MAX;
+    }
+    if (t < 32) {
+        const int64_t r = c * 32 + t;
+        v[512 + t] = r < rows ? static_cast<int>(r + halo_lo) : INT_MAX;
+    }
+    __syncthreads();
+    // bitonic sort, 1024 keys
+    for (int k = 2; k <= 1024; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = t; i < 1024; i += 256) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const int a = v[i], b = v[ixj];
+                    if ((a > b) == up) {
+                        v[i] = b;
+                        v[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (t == 0) {
+        int n = 0, rowsum = 0, bad = 0;
+        int cs = -1, ce = -1;  // current run [cs, ce]
+        for (int i = 0; i < 1024 && v[i] != INT_MAX; ++i) {
+            const int e = v[i];
+            if (cs >= 0 && e <= ce) continue;  // duplicate
+            if (cs >= 0 && e - ce - 1 < kStageGap) {
+                ce = e;
+                continue;
+            }
+            if (cs >= 0) {
+                if (n < kStageRuns) runs[n] = make_int4(cs, ce - cs + 1, rowsum, 0);
+                rowsum += ce - cs + 1;
+                ++n;
+            }
+            cs = ce = e;
+        }
+        if (cs >= 0) {
+            if (n < kStageRuns) runs[n] = make_int4(cs, ce - cs + 1, rowsum, 0);
+            rowsum += ce - cs + 1;
+            ++n;
+        }
+        if (n > kStageRuns || rowsum > 65535) bad = 1;
+        nruns_s = n;
+        nrows_s = rowsum;
+        bad_s = bad;
+        if (bad) atomicExch(overflow, 1);
+        atomicMax(max_rows, rowsum);
+        meta[c] = make_int2(bad ? 0 : n, rowsum);
+    }
+    __syncthreads();
+    if (bad_s) return;
+    const int n = nruns_s;
+    for (int k = t; k < n; k += 256) runs_out[c * kStageRuns + k] = runs[k];
+    auto local = [&](int e) -> unsigned short {
+        int lo = 0, hi = n - 1;  // last run with start <= e
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (runs[mid].x <= e) lo = mid; else hi = mid - 1;
+        }
+        return static_cast<unsigned short>(runs[lo].z + (e - runs[lo].x));
+    };
+    for (int e = t; e < 512; e += 256) {
+        const int l = e >> 4, j = e & 15;
+        unsigned short out = 0xFFFF;
+        if (j < w) {
+            const int col = cols[base + static_cast<int64_t>(j) * 32 + l];
+            if (col >= 0) out = local(col);
+        }
+        lcol[c * 512 + e] = out;
+    }
+    if (t < 32) {
+        const int64_t r = c * 32 + t;
+        lown[c * 32 + t] = r < rows ? local(static_cast<int>(r + halo_lo)) : 0xFFFF;
+    }
+}
+
 template <class M>
 __global__ void sell_fill_kernel(const int64_t* __restrict__ offs, const int64_t* __restrict__ gcols,
                                  const M* __restrict__ gvals, int64_t rows,
@@ -790,6 +1102,74 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     auto kernel = tma ? step_tma_kernel<CPLX, T, KIND, DMODE, MW>
                       : step_kernel<CPLX, T, KIND, DMODE, 0>;
     int used_total = 0;
+    if constexpr (MAXW > 0) {
+        // staged-gather kernel: one 512-byte row slot, plan present and fitting shared memory
+        if (ctx.kernel_variant == 2 && tma && units == 32 && pitch == 32 && a.stage_max_rows > 0 &&
+            nrows > 0) {
+            const size_t stage = static_cast<size_t>(a.stage_max_rows) * 32 * sizeof(T) +
+                                 32 * MAXW * sizeof(typename Ops<CPLX, T>::M) + 1024 + 64;
+            const int nstage = 3 * stage <= 225 * 1024 ? 3 : 2;
+            const size_t smem = nstage * stage;
+            if (smem <= 225 * 1024) {
+                auto sk = step_stage_kernel<CPLX, T, KIND, DMODE, MAXW>;
+                static thread_local std::map<const void*, size_t> attr_set;
+                auto& cur = attr_set[reinterpret_cast<const void*>(sk)];
+                if (cur < smem) {
+                    CFD_CUDA(cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(smem)));
+                    cur = smem;
+                }
+                const int64_t need = ((s.row1 + 31) >> 5) - (s.row0 >> 5);
+                const int grid =
+                    static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, ctx.num_sms)));
+                StepParams p{};
+                p.chunk_ptr = a.chunk_ptr.as<int64_t>();
+                p.chunk_full = a.chunk_full.as<unsigned char>();
+                p.cols = a.cols.as<int>();
+                p.vals = a.vals.p;
+                p.svals = svals;
+                p.row0 = s.row0;
+                p.row1 = s.row1;
+                p.halo_lo = a.part.halo_lo;
+                p.pitch = pitch;
+                p.u_off = 0;
+                p.US = 32;
+                p.R = 8;
+                p.in = s.in;
+                p.w = s.w;
+                p.x = s.x;
+                p.x0 = s.x0;
+                p.alpha = s.alpha;
+                p.beta = s.beta;
+                p.c0 = s.c0;
+                p.c1 = s.c1;
+                p.c2 = s.c2;
+                p.coeff_dev = s.coeff_dev;
+                p.coeff_index = s.coeff_index;
+                p.dots_out = s.dots_out;
+                p.dots_row_stride = static_cast<int64_t>(units) * Ops<CPLX, T>::kCols;
+                if (NDOT > 0) {
+                    const size_t need_bytes =
+                        static_cast<size_t>(s.partial_base + grid) * NDOT * 32 * sizeof(T);
+                    ctx.partials.ensure(std::max<size_t>(need_bytes, 1 << 20));
+                    ctx.counter.ensure(256);
+                }
+                p.partials = ctx.partials.p;
+                p.part_base = s.partial_base;
+                p.nparts = s.partial_base + grid;
+                p.final_launch = s.final_launch ? 1 : 0;
+                p.counter = ctx.counter.as<unsigned>();
+                const StagePlan sp{a.stage_runs.as<int4>(), a.stage_meta.as<int2>(),
+                                   a.stage_lcol.as<unsigned short>(),
+                                   a.stage_lown.as<unsigned short>(), a.stage_max_rows, nstage};
+                sk<<<grid, 256, smem, st>>>(p, sp);
+                CFD_CUDA(cudaGetLastError());
+                ctx.launches++;
+                if (s.grid_used) *s.grid_used = grid;
+                return;
+            }
+        }
+    }
     // column slabs of at most `slab` units (one CTA row-group spans a slab)
     const int slab = ctx.slab_units > 0 ? std::min(ctx.slab_units, 256) : 256;
     for (int u0 = 0; u0 < units; u0 += slab) {
@@ -1090,6 +1470,25 @@ void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d
     CFD_CUDA(cudaMemcpyAsync(&err, dmax.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
     CFD_CUDA(cudaStreamSynchronize(st));
     if (err) fail(CHEBFD_ERR_UNSUPPORTED, "matrix column outside this rank's rows and halos");
+    // staged-gather plan (kernel variant 2): rows of width <= 16 only
+    m.stage_max_rows = 0;
+    if (m.nchunks > 0 && maxlen <= 16 && m.part.ext_rows() < (1LL << 31)) {
+        m.stage_runs.ensure(sizeof(int4) * kStageRuns * static_cast<size_t>(m.nchunks));
+        m.stage_meta.ensure(sizeof(int2) * static_cast<size_t>(m.nchunks));
+        m.stage_lcol.ensure(sizeof(unsigned short) * 512 * static_cast<size_t>(m.nchunks));
+        m.stage_lown.ensure(sizeof(unsigned short) * 32 * static_cast<size_t>(m.nchunks));
+        DeviceBuffer flags(sizeof(int) * 2);
+        CFD_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 2, st));
+        stage_plan_kernel<<<static_cast<unsigned>(m.nchunks), 256, 0, st>>>(
+            m.chunk_ptr.as<int64_t>(), m.cols.as<int>(), rows, m.part.halo_lo,
+            m.stage_runs.as<int4>(), m.stage_meta.as<int2>(), m.stage_lcol.as<unsigned short>(),
+            m.stage_lown.as<unsigned short>(), flags.as<int>(), flags.as<int>() + 1);
+        CFD_CUDA(cudaGetLastError());
+        int h[2] = {0, 0};
+        CFD_CUDA(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CFD_CUDA(cudaStreamSynchronize(st));
+        m.stage_max_rows = h[1] ? 0 : h[0];
+    }
 }
 
 }  // namespace cfd

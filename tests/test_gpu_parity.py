@@ -279,3 +279,39 @@ def test_streamed_randomize_matches_reference_stream(ctx, cplx):
     X = cf.BlockVector(A, nb).randomize(11)
     want = cf.host_randomize(A.dim(), nb, 11, cplx)
     assert bits_equal(X.to_numpy(), want)
+
+
+STAGE_CASES = [("ti", (4, 4, 4), 32, "periodic_xy_open_z"), ("ti", (3, 5, 4), 32, "open_all"),
+               ("graphene", (16, 16), 64, "periodic_xy_open_z"),
+               ("graphene", (13, 7), 64, "open_all")]
+
+
+@pytest.mark.parametrize("name,l,nb,boundary", STAGE_CASES)
+def test_staged_kernel_bitexact(ctx, orc, name, l, nb, boundary):
+    """Kernel variant 2 (gathered rows staged in shared memory by TMA, per-chunk
+    plan): apply_filter X bit-exact with moments, fused W/X bit-exact with dots,
+    on full, padded (open boundaries) and partial chunks."""
+    cx = name == "ti"
+    if cx:
+        A, c = ti(ctx, orc, l, boundary=boundary)
+    else:
+        A, c = graphene(ctx, orc, *l, boundary=boundary)
+    assert A.info["stage_rows"] > 0
+    ctx.set_option("kernel", "stage")
+    try:
+        bounds = (-5.6, 5.6) if cx else (-3.2, 3.3)
+        p = cf.make_filter((-0.2, 0.3), bounds, 24, "lanczos2")
+        x0 = orc.randomize(c.dim, nb, 9, cx)
+        X = block(A, x0)
+        mom = cf.apply_filter(A, X, p, want_moments=True)
+        xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+        assert bits_equal(X.to_numpy(), xr)
+        assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
+        u, w, x = (orc.randomize(c.dim, nb, s, cx) for s in (1, 2, 3))
+        U, W, Xb = block(A, u), block(A, w), block(A, x)
+        d = cf.spmmvm_fused(A, U, W, Xb, p.alpha, p.beta, 0.83, dots=True)
+        dref = orc.spmmvm_fused(c, u, w, x, p.alpha, p.beta, 0.83, want_dots=True)
+        assert bits_equal(W.to_numpy(), w) and bits_equal(Xb.to_numpy(), x)
+        assert np.allclose(d, dref, rtol=1e-12, atol=1e-12 * np.max(np.abs(dref)))
+    finally:
+        ctx.set_option("kernel", "tma")
