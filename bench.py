@@ -344,7 +344,7 @@ def main():
     ap.add_argument("--nb", type=int, default=32)
     ap.add_argument("--degree", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--kernel", default="tma", choices=["tma", "gather", "stage"],
+    ap.add_argument("--kernel", default="tma", choices=["tma", "gather", "stage", "tma2"],
                     help="step kernel: TMA-staged SELL chunks (default) or plain register gathers")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

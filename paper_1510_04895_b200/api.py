@@ -158,7 +158,7 @@ class Context:
         slab_units (int, 0 = 256)."""
         code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5}[name]
         if name == "kernel" and isinstance(value, str):
-            value = {"gather": 0, "tma": 1, "stage": 2}[value]
+            value = {"gather": 0, "tma": 1, "stage": 2, "tma2": 3}[value]
         _check(_lib().chebfd_ctx_set_option(self._h, code, int(value)))
 
 

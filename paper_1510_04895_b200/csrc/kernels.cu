@@ -146,6 +146,17 @@ __device__ __forceinline__ double2 tadd<double2>(double2 a, double2 b) {
     return make_double2(add(a.x, b.x), add(a.y, b.y));
 }
 
+// L2-coherent load of a partial (double, double2, or a pair of double2 units)
+template <class T>
+__device__ __forceinline__ T ldcg_t(const T* p) {
+    if constexpr (std::is_same_v<T, double> || std::is_same_v<T, double2>) {
+        return __ldcg(p);
+    } else {
+        const double2* q = reinterpret_cast<const double2*>(p);
+        return T{__ldcg(q), __ldcg(q + 1)};
+    }
+}
+
 // ---- fixed-order block + grid reduction of NDOT per-unit accumulators -------------
 // Threads are laid out t = rr*US + u.  Each CTA writes NDOT*US partials; the
 // last CTA to finish (ticket) sums partial rows [0, nparts) in order and
@@ -183,7 +194,7 @@ __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1],
         T s = T{};
         bool first = true;
         for (int q = rr; q < nparts; q += R) {
-            const T v = __ldcg(&partials[(static_cast<int64_t>(q) * NDOT + d) * US + u]);
+            const T v = ldcg_t(&partials[(static_cast<int64_t>(q) * NDOT + d) * US + u]);
             s = first ? v : tadd(s, v);
             first = false;
         }
@@ -587,6 +598,259 @@ __global__ void __launch_bounds__(256, CFD_TMA_MINB) step_tma_kernel(const StepP
                                  else
                                      O::store_re(static_cast<double*>(outp) + d * dstride,
                                                  uoff + uu, vv);
+                             });
+    }
+}
+
+// ---- two units per thread, 256-bit accesses, W / X staged by TMA (default where it applies) ----
+// Same arithmetic and order as step_tma_kernel, but each thread owns two
+// adjacent 16-byte units of its row: the eleven gathers are LDG.256 (32 B per
+// thread, 512 B per half warp), so a row in flight costs half the threads; the
+// own-row streams W / X (/ x0) of the tile come into shared memory by one TMA
+// bulk copy each with the matrix chunk, so no register holds them while the
+// gathers are in flight.  Net: about twice the rows in flight per SM at the
+// same register budget (the TMA kernel's limit), and half the load instructions.
+template <class T>
+struct alignas(32) U2 {
+    T a, b;
+};
+template <>
+__device__ __forceinline__ U2<double2> tadd<U2<double2>>(U2<double2> x, U2<double2> y) {
+    return {tadd(x.a, y.a), tadd(x.b, y.b)};
+}
+__device__ __forceinline__ U2<double2> ld256_nc(const double2* p) {
+    U2<double2> v;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.a.x), "=d"(v.a.y), "=d"(v.b.x), "=d"(v.b.y)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st256_cs(double2* p, const U2<double2>& v) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.a.x), "d"(v.a.y),
+                 "d"(v.b.x), "d"(v.b.y)
+                 : "memory");
+}
+
+// the per-unit epilogue of step_epilogue, on values already in registers,
+// returning what step_epilogue stores (so the two units store as one 256-bit op)
+template <class O, class T, int KIND, int DMODE, int NA>
+__device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, const T xi,
+                                          const T x0v, T& w_out, T& x_out, T& x0_out, double beta,
+                                          double coeff, double c1, double c2, T (&acc_d)[NA],
+                                          T (&comp_d)[NA]) {
+    if constexpr (KIND == kStepSpmmvm) {
+        T y = acc;
+        if (beta != 0.0) y = O::vadd(y, O::smul(beta, ui));  // kernels.hpp:62-65
+        w_out = y;
+        if constexpr (DMODE == 3) {
+            x0_out = ui;
+            acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, ui));
+            acc_d[1] = O::vadd(acc_d[1], O::cdot(ui, y));
+        }
+    } else if constexpr (KIND == kStepStart2) {
+        T wr = acc;
+        if (beta != 0.0) wr = O::vadd(wr, O::smul(beta, ui));
+        const T wn = O::vadd(O::vadd(O::smul(1.0, wr), O::smul(-1.0, xi)), O::smul(0.0, xi));
+        w_out = wn;
+        if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(xi, wn));
+        x_out = O::vadd(O::vadd(O::smul(coeff, xi), O::smul(c1, ui)), O::smul(c2, wn));
+    } else {
+        const T wn = O::vsub(O::vadd(acc, O::smul(beta, ui)), wi);
+        w_out = wn;
+        if constexpr (KIND == kStepFused) {
+            if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
+            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+            x_out = O::vadd(xi, O::smul(coeff, wn));
+        } else {
+            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+        }
+    }
+}
+
+template <bool CPLX, int KIND, int DMODE, int MAXW>
+__global__ void __launch_bounds__(256, (MAXW <= 8 ? 2 : 1)) step_tma2_kernel(const StepParams p) {
+    using T = double2;
+    using O = Ops<CPLX, T>;
+    using M = typename O::M;
+    using P = U2<T>;
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
+    constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
+    constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
+    constexpr int NS = (HAS_W ? 1 : 0) + (HAS_X ? 1 : 0) + (HAS_X0 ? 1 : 0);  // staged streams
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2];
+    const int t = threadIdx.x;
+    const int HS = p.US >> 1;  // threads per row
+    const int rr = t / HS;
+    const int u2 = t - rr * HS;
+    const int R = p.R;          // rows per pass
+    constexpr int TR = 32;      // one chunk per tile
+    const int pitch = p.pitch;  // == p.US (whole rows)
+    const int cap = MAXW * TR;
+    const size_t sell_bytes = ((cap * sizeof(int) + 15) & ~size_t(15)) + cap * sizeof(M);
+    const size_t row_tile = static_cast<size_t>(TR) * pitch * sizeof(T);
+    const size_t stage_bytes = sell_bytes + NS * row_tile;
+    auto cols_s = [&](int b) { return reinterpret_cast<const int*>(smem_raw + b * stage_bytes); };
+    auto vals_s = [&](int b) {
+        return reinterpret_cast<const M*>(smem_raw + b * stage_bytes +
+                                          ((cap * sizeof(int) + 15) & ~size_t(15)));
+    };
+    auto rows_s = [&](int b, int k) {
+        return reinterpret_cast<const T*>(smem_raw + b * stage_bytes + sell_bytes + k * row_tile);
+    };
+
+    const int cu = 2 * u2;
+    const T* __restrict__ inu = static_cast<const T*>(p.in) + cu;
+    T* __restrict__ W = static_cast<T*>(p.w);
+    T* __restrict__ X = static_cast<T*>(p.x);
+    T* __restrict__ X0 = static_cast<T*>(p.x0);
+    const M* __restrict__ gvals = static_cast<const M*>(p.svals);
+    const int64_t halo = p.halo_lo;
+    double coeff = p.c0, c1 = p.c1, c2 = p.c2;
+    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepStart2 && p.coeff_dev) {
+        coeff = p.coeff_dev[0];
+        c1 = p.coeff_dev[1];
+        c2 = p.coeff_dev[2];
+    }
+    P acc_d[NDOT > 0 ? NDOT : 1];
+    P comp_d[NDOT > 0 ? NDOT : 1];
+#pragma unroll
+    for (int d = 0; d < (NDOT > 0 ? NDOT : 1); ++d) {
+        acc_d[d] = P{O::zero(), O::zero()};
+        comp_d[d] = P{O::zero(), O::zero()};
+    }
+    const int64_t row0 = p.row0, row1 = p.row1;
+    const int64_t cbeg = row0 >> 5;
+    const int64_t ntiles = row1 > row0 ? ((row1 + 31) >> 5) - cbeg : 0;
+    const int64_t* __restrict__ cptr = p.chunk_ptr;
+
+    auto issue = [&](int64_t tile, int b) {
+        const int64_t c = cbeg + tile;
+        const int64_t s0 = cptr[c], s1 = cptr[c + 1];
+        const unsigned n = static_cast<unsigned>(s1 - s0);
+        const int64_t ra = max(c * 32, row0), rb = min(c * 32 + 32, row1);
+        const unsigned rows_b = static_cast<unsigned>((rb - ra) * pitch * sizeof(T));
+        unsigned char* base = smem_raw + b * stage_bytes;
+        mbar_arrive_expect_tx(&bars[b], n * 4u + n * static_cast<unsigned>(sizeof(M)) + NS * rows_b);
+        if (n) {
+            tma_load_1d(base, p.cols + s0, n * 4u, &bars[b]);
+            tma_load_1d(base + ((cap * sizeof(int) + 15) & ~size_t(15)), gvals + s0,
+                        n * static_cast<unsigned>(sizeof(M)), &bars[b]);
+        }
+        const size_t off = static_cast<size_t>(ra - c * 32) * pitch * sizeof(T);
+        int k = 0;
+        if constexpr (HAS_W) tma_load_1d(base + sell_bytes + (k++) * row_tile + off, W + ra * pitch, rows_b, &bars[b]);
+        if constexpr (HAS_X) tma_load_1d(base + sell_bytes + (k++) * row_tile + off, X + ra * pitch, rows_b, &bars[b]);
+        if constexpr (HAS_X0) tma_load_1d(base + sell_bytes + (k++) * row_tile + off, X0 + ra * pitch, rows_b, &bars[b]);
+        (void)k;
+    };
+
+    auto row = [&](auto fast_tag, int64_t r, int64_t c, int64_t sbase, int b) {
+        constexpr bool FAST = decltype(fast_tag)::value;
+        const int* cs = cols_s(b);
+        const M* vs = vals_s(b);
+        const int lane = static_cast<int>(r & 31);
+        int coff, w;
+        if constexpr (FAST) {
+            coff = lane;
+            w = MAXW;
+        } else {
+            const int64_t cb = __ldg(&cptr[c]);
+            coff = static_cast<int>(cb - sbase) + lane;
+            w = static_cast<int>((__ldg(&cptr[c + 1]) - cb) >> 5);
+        }
+        P acc{O::zero(), O::zero()};
+        int cc[MAXW];
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j) cc[j] = (FAST || j < w) ? cs[coff + j * 32] : -1;
+        P g[MAXW];
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j)
+            if (FAST || cc[j] >= 0) g[j] = ld256_nc(&inu[static_cast<int64_t>(cc[j]) * pitch]);
+#pragma unroll
+        for (int j = 0; j < MAXW; ++j)
+            if (FAST || cc[j] >= 0) {
+                const M v = vs[coff + j * 32];
+                acc.a = O::vadd(acc.a, O::prod(v, g[j].a));
+                acc.b = O::vadd(acc.b, O::prod(v, g[j].b));
+            }
+        const P ui = ld256_nc(&inu[(r + halo) * pitch]);
+        const int lr = static_cast<int>(r - c * 32);
+        P wi{}, xi{}, x0v{};
+        int k = 0;
+        if constexpr (HAS_W) wi = *reinterpret_cast<const P*>(rows_s(b, k++) + lr * pitch + cu);
+        if constexpr (HAS_X) xi = *reinterpret_cast<const P*>(rows_s(b, k++) + lr * pitch + cu);
+        if constexpr (HAS_X0) x0v = *reinterpret_cast<const P*>(rows_s(b, k++) + lr * pitch + cu);
+        (void)k;
+        P wo{}, xo{}, x0o{};
+        T ad_a[NDOT > 0 ? NDOT : 1], cd_a[NDOT > 0 ? NDOT : 1], ad_b[NDOT > 0 ? NDOT : 1],
+            cd_b[NDOT > 0 ? NDOT : 1];
+#pragma unroll
+        for (int d = 0; d < (NDOT > 0 ? NDOT : 1); ++d) {
+            ad_a[d] = acc_d[d].a;
+            cd_a[d] = comp_d[d].a;
+            ad_b[d] = acc_d[d].b;
+            cd_b[d] = comp_d[d].b;
+        }
+        epilogue2<O, T, KIND, DMODE>(acc.a, ui.a, wi.a, xi.a, x0v.a, wo.a, xo.a, x0o.a, p.beta,
+                                     coeff, c1, c2, ad_a, cd_a);
+        epilogue2<O, T, KIND, DMODE>(acc.b, ui.b, wi.b, xi.b, x0v.b, wo.b, xo.b, x0o.b, p.beta,
+                                     coeff, c1, c2, ad_b, cd_b);
+#pragma unroll
+        for (int d = 0; d < (NDOT > 0 ? NDOT : 1); ++d) {
+            acc_d[d] = P{ad_a[d], ad_b[d]};
+            comp_d[d] = P{cd_a[d], cd_b[d]};
+        }
+        const int64_t own = r * pitch + cu;
+        st256_cs(&W[own], wo);
+        if constexpr (KIND == kStepSpmmvm && DMODE == 3) st256_cs(&X0[own], x0o);
+        if constexpr (KIND == kStepFused || KIND == kStepStart2) st256_cs(&X[own], xo);
+    };
+
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    int64_t tile = blockIdx.x;
+    if (t == 0 && tile < ntiles) issue(tile, 0);
+    unsigned phases = 0u;
+    for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+        const int buf = k & 1;
+        if (t == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
+        const int64_t c = cbeg + tile;
+        const int64_t sbase = cptr[c];
+        const bool fast = (cptr[c + 1] - sbase) == 32 * MAXW && c * 32 >= row0 && c * 32 + 32 <= row1 &&
+                          __ldg(&p.chunk_full[c]) != 0;
+        mbar_wait(&bars[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        if (fast) {
+            for (int it = 0; it < TR; it += R) row(std::true_type{}, c * 32 + it + rr, c, sbase, buf);
+        } else {
+            for (int it = 0; it < TR; it += R) {
+                const int64_t r = c * 32 + it + rr;
+                if (r < row0 || r >= row1) continue;
+                row(std::false_type{}, r, c, sbase, buf);
+            }
+        }
+        __syncthreads();
+    }
+
+    if constexpr (NDOT > 0) {
+        void* outp = p.dots_out;
+        const int64_t dstride = p.dots_row_stride;
+        grid_reduce<P, NDOT>(acc_d, R, HS, reinterpret_cast<P*>(p.partials), p.part_base + blockIdx.x,
+                             p.nparts, p.final_launch != 0, p.counter, [&](int d, int uu, P vv) {
+                                 if (DMODE == 1) {
+                                     O::store_full(static_cast<T*>(outp), 2 * uu, vv.a);
+                                     O::store_full(static_cast<T*>(outp), 2 * uu + 1, vv.b);
+                                 } else {
+                                     O::store_re(static_cast<double*>(outp) + d * dstride, 2 * uu, vv.a);
+                                     O::store_re(static_cast<double*>(outp) + d * dstride, 2 * uu + 1, vv.b);
+                                 }
                              });
     }
 }
@@ -1168,6 +1432,84 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
                 if (s.grid_used) *s.grid_used = grid;
                 return;
             }
+        }
+    }
+    if constexpr (MAXW > 0 && std::is_same_v<T, double2>) {
+        // two units per thread: whole rows of 16 or 32 units (one chunk per tile)
+        // default for short rows (graphene: +1..3 %, measured); TI's 11-entry rows keep
+        // step_tma_kernel (the 2-unit gathers cost registers: 0.70 vs 0.61 ms on C2)
+        const bool pick = ctx.kernel_variant == 3 || (ctx.kernel_variant == 1 && MAXW <= 8);
+        if (pick && tma && units == pitch && (units == 16 || units == 32) && nrows > 0) {
+            constexpr int NDOT2 = NDOT;
+            constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
+            constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
+            constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
+            constexpr int NS = (HAS_W ? 1 : 0) + (HAS_X ? 1 : 0) + (HAS_X0 ? 1 : 0);
+            using M = typename Ops<CPLX, T>::M;
+            const size_t cap = static_cast<size_t>(MAXW) * 32;
+            const size_t stage = ((cap * sizeof(int) + 15) & ~size_t(15)) + cap * sizeof(M) +
+                                 static_cast<size_t>(NS) * 32 * pitch * sizeof(T);
+            const int HS = units / 2, R = 256 / HS;
+            const size_t smem = std::max(2 * stage, static_cast<size_t>(NDOT2) * 256 * 2 * sizeof(T));
+            auto k2 = step_tma2_kernel<CPLX, KIND, DMODE, MAXW>;
+            if (smem > 48 * 1024) {
+                static thread_local std::map<const void*, size_t> attr_set;
+                auto& cur = attr_set[reinterpret_cast<const void*>(k2)];
+                if (cur < smem) {
+                    CFD_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(smem)));
+                    cur = smem;
+                }
+            }
+            static thread_local std::map<std::pair<const void*, size_t>, int> occ2;
+            auto key = std::make_pair(reinterpret_cast<const void*>(k2), smem);
+            auto it = occ2.find(key);
+            const int maxb = it != occ2.end() ? it->second
+                                              : (occ2[key] = max_blocks_for(k2, 256, smem, ctx.num_sms));
+            const int64_t need = ((s.row1 + 31) >> 5) - (s.row0 >> 5);
+            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, maxb)));
+            StepParams p{};
+            p.chunk_ptr = a.chunk_ptr.as<int64_t>();
+            p.chunk_full = a.chunk_full.as<unsigned char>();
+            p.cols = a.cols.as<int>();
+            p.vals = a.vals.p;
+            p.svals = svals;
+            p.row0 = s.row0;
+            p.row1 = s.row1;
+            p.halo_lo = a.part.halo_lo;
+            p.pitch = pitch;
+            p.u_off = 0;
+            p.US = units;
+            p.R = R;
+            p.in = s.in;
+            p.w = s.w;
+            p.x = s.x;
+            p.x0 = s.x0;
+            p.alpha = s.alpha;
+            p.beta = s.beta;
+            p.c0 = s.c0;
+            p.c1 = s.c1;
+            p.c2 = s.c2;
+            p.coeff_dev = s.coeff_dev;
+            p.coeff_index = s.coeff_index;
+            p.dots_out = s.dots_out;
+            p.dots_row_stride = static_cast<int64_t>(units) * Ops<CPLX, T>::kCols;
+            if (NDOT > 0) {
+                const size_t need_bytes =
+                    static_cast<size_t>(s.partial_base + grid) * NDOT * units * sizeof(T);
+                ctx.partials.ensure(std::max<size_t>(need_bytes, 1 << 20));
+                ctx.counter.ensure(256);
+            }
+            p.partials = ctx.partials.p;
+            p.part_base = s.partial_base;
+            p.nparts = s.partial_base + grid;
+            p.final_launch = s.final_launch ? 1 : 0;
+            p.counter = ctx.counter.as<unsigned>();
+            k2<<<grid, 256, smem, st>>>(p);
+            CFD_CUDA(cudaGetLastError());
+            ctx.launches++;
+            if (s.grid_used) *s.grid_used = grid;
+            return;
         }
     }
     // column slabs of at most `slab` units (one CTA row-group spans a slab)

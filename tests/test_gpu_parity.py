@@ -282,22 +282,25 @@ def test_streamed_randomize_matches_reference_stream(ctx, cplx):
 
 
 STAGE_CASES = [("ti", (4, 4, 4), 32, "periodic_xy_open_z"), ("ti", (3, 5, 4), 32, "open_all"),
+               ("ti", (4, 4, 5), 16, "periodic_all"),
                ("graphene", (16, 16), 64, "periodic_xy_open_z"),
-               ("graphene", (13, 7), 64, "open_all")]
+               ("graphene", (13, 7), 64, "open_all"), ("graphene", (16, 8), 32, "open_all")]
 
 
+@pytest.mark.parametrize("kernel", ["stage", "tma2"])
 @pytest.mark.parametrize("name,l,nb,boundary", STAGE_CASES)
-def test_staged_kernel_bitexact(ctx, orc, name, l, nb, boundary):
-    """Kernel variant 2 (gathered rows staged in shared memory by TMA, per-chunk
-    plan): apply_filter X bit-exact with moments, fused W/X bit-exact with dots,
-    on full, padded (open boundaries) and partial chunks."""
+def test_staged_kernel_bitexact(ctx, orc, name, l, nb, boundary, kernel):
+    """Kernel variants 2 (gathered rows staged in shared memory by TMA, per-chunk
+    plan) and 3 (two units per thread, 256-bit accesses, W/X staged by TMA):
+    apply_filter X bit-exact with moments, fused W/X bit-exact with dots, on
+    full, padded (open boundaries) and partial chunks."""
     cx = name == "ti"
     if cx:
         A, c = ti(ctx, orc, l, boundary=boundary)
     else:
         A, c = graphene(ctx, orc, *l, boundary=boundary)
     assert A.info["stage_rows"] > 0
-    ctx.set_option("kernel", "stage")
+    ctx.set_option("kernel", kernel)
     try:
         bounds = (-5.6, 5.6) if cx else (-3.2, 3.3)
         p = cf.make_filter((-0.2, 0.3), bounds, 24, "lanczos2")

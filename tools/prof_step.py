@@ -15,7 +15,7 @@ import paper_1510_04895_b200 as cf  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--kernel", default="tma", choices=["gather", "tma", "stage"])
+    ap.add_argument("--kernel", default="tma", choices=["gather", "tma", "stage", "tma2"])
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--lattice", type=int, default=64)
     ap.add_argument("--nb", type=int, default=32)
