@@ -668,7 +668,7 @@ __device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, c
 }
 
 template <bool CPLX, int KIND, int DMODE, int MAXW>
-__global__ void __launch_bounds__(256, (MAXW <= 8 ? 2 : 1)) step_tma2_kernel(const StepParams p) {
+__global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
     using T = double2;
     using O = Ops<CPLX, T>;
     using M = typename O::M;
@@ -1366,7 +1366,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     auto kernel = tma ? step_tma_kernel<CPLX, T, KIND, DMODE, MW>
                       : step_kernel<CPLX, T, KIND, DMODE, 0>;
     int used_total = 0;
-    if constexpr (MAXW > 0) {
+    if constexpr (MAXW >= 8 && std::is_same_v<T, double2>) {
         // staged-gather kernel: one 512-byte row slot, plan present and fitting shared memory
         if (ctx.kernel_variant == 2 && tma && units == 32 && pitch == 32 && a.stage_max_rows > 0 &&
             nrows > 0) {
@@ -1434,7 +1434,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
             }
         }
     }
-    if constexpr (MAXW > 0 && std::is_same_v<T, double2>) {
+    if constexpr (MAXW > 0 && MAXW <= 8 && std::is_same_v<T, double2>) {
         // two units per thread: whole rows of 16 or 32 units (one chunk per tile)
         // default for short rows (graphene: +1..3 %, measured); TI's 11-entry rows keep
         // step_tma_kernel (the 2-unit gathers cost registers: 0.70 vs 0.61 ms on C2)

@@ -281,19 +281,21 @@ def test_streamed_randomize_matches_reference_stream(ctx, cplx):
     assert bits_equal(X.to_numpy(), want)
 
 
-STAGE_CASES = [("ti", (4, 4, 4), 32, "periodic_xy_open_z"), ("ti", (3, 5, 4), 32, "open_all"),
-               ("ti", (4, 4, 5), 16, "periodic_all"),
-               ("graphene", (16, 16), 64, "periodic_xy_open_z"),
-               ("graphene", (13, 7), 64, "open_all"), ("graphene", (16, 8), 32, "open_all")]
+STAGE_CASES = [("ti", (4, 4, 4), 32, "periodic_xy_open_z", "stage"),
+               ("ti", (3, 5, 4), 32, "open_all", "stage"),
+               ("graphene", (16, 16), 64, "periodic_xy_open_z", "tma2"),
+               ("graphene", (13, 7), 64, "open_all", "tma2"),
+               ("graphene", (16, 8), 32, "open_all", "tma2"),
+               ("graphene", (16, 8), 32, "periodic_all", "tma")]
 
 
-@pytest.mark.parametrize("kernel", ["stage", "tma2"])
-@pytest.mark.parametrize("name,l,nb,boundary", STAGE_CASES)
+@pytest.mark.parametrize("name,l,nb,boundary,kernel", STAGE_CASES)
 def test_staged_kernel_bitexact(ctx, orc, name, l, nb, boundary, kernel):
     """Kernel variants 2 (gathered rows staged in shared memory by TMA, per-chunk
-    plan) and 3 (two units per thread, 256-bit accesses, W/X staged by TMA):
-    apply_filter X bit-exact with moments, fused W/X bit-exact with dots, on
-    full, padded (open boundaries) and partial chunks."""
+    plan; rows of >= 8 entries) and 3 / default for short rows (two units per
+    thread, 256-bit accesses, W/X staged by TMA): apply_filter X bit-exact with
+    moments, fused W/X bit-exact with dots, on full, padded (open boundaries)
+    and partial chunks."""
     cx = name == "ti"
     if cx:
         A, c = ti(ctx, orc, l, boundary=boundary)
