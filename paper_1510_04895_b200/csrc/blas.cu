@@ -92,11 +92,12 @@ void mult_small_dev_b(Context& c, const Block& x, const void* b_dev, int64_t bco
 
 void mult_small_host_b(Context& c, const Block& x, const void* b_host, int64_t bcols, Block& y) {
     const size_t bytes = static_cast<size_t>(x.width * bcols) * x.scalar_bytes();
-    DeviceBuffer b(std::max<size_t>(bytes, 16));
+    DeviceBuffer& b = c.small[2];
+    b.ensure(std::max<size_t>(bytes, 16));
     if (bytes)
         CFD_CUDA(cudaMemcpyAsync(b.p, b_host, bytes, cudaMemcpyHostToDevice, c.stream));
     mult_small_dev_b(c, x, b.p, bcols, y);
-    ctx_sync(c);  // b is freed on return
+    ctx_sync(c);  // b_host may be released by the caller
 }
 
 bool heev_host(Context& c, int kind, int64_t n64, const void* a_rowmajor, double* w, void* v_rowmajor,
@@ -117,32 +118,35 @@ bool heev_host(Context& c, int kind, int64_t n64, const void* a_rowmajor, double
                 acol[i + static_cast<size_t>(j) * n] = a[static_cast<size_t>(i) * n + j];
             }
         }
-    DeviceBuffer da(sb * n * n), dw(sizeof(double) * n), dinfo(sizeof(int));
+    DeviceBuffer& da = c.small[3];
+    da.ensure(sb * n * n + sizeof(double) * n + 16);
+    double* dw_p = reinterpret_cast<double*>(static_cast<char*>(da.p) + sb * n * n);
+    int* dinfo_p = reinterpret_cast<int*>(dw_p + n);
     CFD_CUDA(cudaMemcpyAsync(da.p, acol.data(), sb * n * n, cudaMemcpyHostToDevice, c.stream));
     const cusolverEigMode_t mode = vectors ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
     int lwork = 0;
     if (kind == CHEBFD_REAL64) {
         if (cusolverDnDsyevd_bufferSize(h, mode, CUBLAS_FILL_MODE_LOWER, n, da.as<double>(), n,
-                                        dw.as<double>(), &lwork) != CUSOLVER_STATUS_SUCCESS)
+                                        dw_p, &lwork) != CUSOLVER_STATUS_SUCCESS)
             fail(CHEBFD_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
         c.workspace.ensure(sizeof(double) * std::max(lwork, 1));
-        if (cusolverDnDsyevd(h, mode, CUBLAS_FILL_MODE_LOWER, n, da.as<double>(), n, dw.as<double>(),
-                             c.workspace.as<double>(), lwork, dinfo.as<int>()) != CUSOLVER_STATUS_SUCCESS)
+        if (cusolverDnDsyevd(h, mode, CUBLAS_FILL_MODE_LOWER, n, da.as<double>(), n, dw_p,
+                             c.workspace.as<double>(), lwork, dinfo_p) != CUSOLVER_STATUS_SUCCESS)
             fail(CHEBFD_ERR_CUDA, "cusolverDnDsyevd failed");
     } else {
         if (cusolverDnZheevd_bufferSize(h, mode, CUBLAS_FILL_MODE_LOWER, n, da.as<cuDoubleComplex>(), n,
-                                        dw.as<double>(), &lwork) != CUSOLVER_STATUS_SUCCESS)
+                                        dw_p, &lwork) != CUSOLVER_STATUS_SUCCESS)
             fail(CHEBFD_ERR_CUDA, "cusolverDnZheevd_bufferSize failed");
         c.workspace.ensure(sizeof(cuDoubleComplex) * std::max(lwork, 1));
         if (cusolverDnZheevd(h, mode, CUBLAS_FILL_MODE_LOWER, n, da.as<cuDoubleComplex>(), n,
-                             dw.as<double>(), c.workspace.as<cuDoubleComplex>(), lwork,
-                             dinfo.as<int>()) != CUSOLVER_STATUS_SUCCESS)
+                             dw_p, c.workspace.as<cuDoubleComplex>(), lwork,
+                             dinfo_p) != CUSOLVER_STATUS_SUCCESS)
             fail(CHEBFD_ERR_CUDA, "cusolverDnZheevd failed");
     }
     c.launches++;
     int info = 0;
-    CFD_CUDA(cudaMemcpyAsync(&info, dinfo.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    CFD_CUDA(cudaMemcpyAsync(w, dw.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    CFD_CUDA(cudaMemcpyAsync(&info, dinfo_p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CFD_CUDA(cudaMemcpyAsync(w, dw_p, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
     if (vectors)
         CFD_CUDA(cudaMemcpyAsync(acol.data(), da.p, sb * n * n, cudaMemcpyDeviceToHost, c.stream));
     ctx_sync(c);

@@ -48,6 +48,53 @@ void DeviceBuffer::ensure(size_t n) {
     bytes = alloc;
 }
 
+void* Context::take_block_mem(size_t bytes) {
+    auto it = block_cache.find(bytes);
+    if (it != block_cache.end()) {
+        void* p = it->second;
+        block_cache.erase(it);
+        block_cache_bytes -= bytes;
+        return p;
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        trim_block_cache();
+        CFD_CUDA(cudaMalloc(&p, bytes));
+    }
+    return p;
+}
+
+void Context::give_block_mem(void* p, size_t bytes) {
+    if (!p) return;
+    if (bytes > block_cache_limit) {
+        cudaFree(p);
+        return;
+    }
+    while (block_cache_bytes + bytes > block_cache_limit && !block_cache.empty()) {
+        auto it = std::prev(block_cache.end());  // drop the largest cached block
+        block_cache_bytes -= it->first;
+        cudaFree(it->second);
+        block_cache.erase(it);
+    }
+    block_cache.emplace(bytes, p);
+    block_cache_bytes += bytes;
+}
+
+void Context::trim_block_cache() {
+    for (auto& kv : block_cache) cudaFree(kv.second);
+    block_cache.clear();
+    block_cache_bytes = 0;
+}
+
+Block::~Block() {
+    if (ctx && buf.p) {
+        ctx->give_block_mem(buf.p, buf.bytes);
+        buf.p = nullptr;
+        buf.bytes = 0;
+    }
+}
+
 Context::~Context() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     graphs.clear();
@@ -62,6 +109,7 @@ Context::~Context() {
     if (stream) cudaStreamDestroy(stream);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (host_pinned) cudaFreeHost(host_pinned);
+    trim_block_cache();
 }
 
 void* Context::pinned(size_t bytes) {
@@ -163,7 +211,8 @@ std::unique_ptr<Block> make_block(Context& c, const Matrix* m, int kind, int64_t
     }
     const size_t bytes = static_cast<size_t>((b->halo_lo + rows + b->halo_hi) * width) *
                          b->scalar_bytes();
-    b->buf.ensure(std::max<size_t>(bytes, 256));
+    b->buf.bytes = std::max<size_t>(bytes, 256);
+    b->buf.p = c.take_block_mem(b->buf.bytes);
     if (zero) {
         CFD_CUDA(cudaMemsetAsync(b->buf.p, 0, b->buf.bytes, c.stream));
     } else {

@@ -129,6 +129,7 @@ struct Block {
     int64_t row_begin = 0, dim_global = 0;
     const Matrix* shape_of = nullptr;  // partition the halos belong to (may be null)
     DeviceBuffer buf;   // (halo_lo + rows + halo_hi) x width scalars
+    ~Block();           // storage goes back to the context's block cache
     size_t scalar_bytes() const { return kind ? 16 : 8; }
     void* base() const { return buf.p; }  // extended row 0
     void* owned() const {
@@ -186,6 +187,16 @@ struct Context {
     DeviceBuffer workspace;  // cuSOLVER / misc
     DeviceBuffer devinfo;
     DeviceBuffer coeffs;     // filter coefficients (device copy)
+    DeviceBuffer small[4];   // host-fed small operands (rotations, eigenvalues, Gram, eig)
+    // exact-size cache of block storage: the solver allocates the same blocks every
+    // iteration, and cudaFree synchronises the device.  All work on a block is
+    // ordered on `stream` (comm work is joined back into it), so reuse needs no
+    // further synchronisation.
+    std::multimap<size_t, void*> block_cache;
+    size_t block_cache_bytes = 0, block_cache_limit = size_t(8) << 30;
+    void* take_block_mem(size_t bytes);
+    void give_block_mem(void* p, size_t bytes);
+    void trim_block_cache();
     void* host_pinned = nullptr;  // small pinned staging
     size_t host_pinned_bytes = 0;
     std::map<GraphKey, GraphEntry> graphs;

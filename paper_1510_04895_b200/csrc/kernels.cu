@@ -191,14 +191,25 @@ __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1],
     __threadfence();
 #pragma unroll
     for (int d = 0; d < NDOT; ++d) {
+        // partials rr, rr + R, rr + 2R, ... summed left to right; eight loads in
+        // flight per step (the order, hence every bit, is the sequential loop's)
+        auto at = [&](int q) {
+            return ldcg_t(&partials[(static_cast<int64_t>(q) * NDOT + d) * US + u]);
+        };
         T s = T{};
-        bool first = true;
-        for (int q = rr; q < nparts; q += R) {
-            const T v = ldcg_t(&partials[(static_cast<int64_t>(q) * NDOT + d) * US + u]);
-            s = first ? v : tadd(s, v);
-            first = false;
+        int q = rr;
+        if (q < nparts) {
+            s = at(q);
+            q += R;
         }
-        if (first) s = T{};
+        for (; q + 7 * R < nparts; q += 8 * R) {
+            T v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = at(q + k * R);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s = tadd(s, v[k]);
+        }
+        for (; q < nparts; q += R) s = tadd(s, at(q));
         sred[d * nthr + t] = s;
     }
     __syncthreads();

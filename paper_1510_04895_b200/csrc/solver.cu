@@ -113,13 +113,15 @@ Ritz rayleigh_ritz(Context& c, const Matrix& a, Block& q) {
         fail(CHEBFD_ERR_RUNTIME, "rayleigh_ritz: projected eigensolve failed");
     out.vectors = make_block(c, &a, q.kind, q.rows, nb, false);
     auto av = make_block(c, &a, q.kind, q.rows, nb, false);
-    DeviceBuffer drot(std::max<size_t>(rot.a.size() * sizeof(double), 16));
+    DeviceBuffer& drot = c.small[0];
+    drot.ensure(std::max<size_t>(rot.a.size() * sizeof(double), 16));
     CFD_CUDA(cudaMemcpyAsync(drot.p, rot.a.data(), rot.a.size() * sizeof(double),
                              cudaMemcpyHostToDevice, c.stream));
     mult_small_dev_b(c, q, drot.p, nb, *out.vectors);
     mult_small_dev_b(c, *aq, drot.p, nb, *av);
     // residual norms ||A v_k - lambda_k v_k|| fused into one reduction pass
-    DeviceBuffer dlam(sizeof(double) * std::max<int64_t>(nb, 1));
+    DeviceBuffer& dlam = c.small[1];
+    dlam.ensure(sizeof(double) * std::max<int64_t>(nb, 1));
     CFD_CUDA(cudaMemcpyAsync(dlam.p, out.values.data(), sizeof(double) * nb, cudaMemcpyHostToDevice,
                              c.stream));
     c.dscratch.ensure(sizeof(double) * nb);
@@ -134,7 +136,8 @@ Ritz rayleigh_ritz(Context& c, const Matrix& a, Block& q) {
 }
 
 void divide_columns(Context& c, Block& b, const std::vector<double>& d) {
-    DeviceBuffer dd(sizeof(double) * std::max<size_t>(d.size(), 1));
+    DeviceBuffer& dd = c.small[1];
+    dd.ensure(sizeof(double) * std::max<size_t>(d.size(), 1));
     CFD_CUDA(cudaMemcpyAsync(dd.p, d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice,
                              c.stream));
     launch_scale_columns(c, b, dd.as<double>(), c.stream);
@@ -516,8 +519,15 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
                 rep->converged = 1;
                 break;
             }
-            x = std::move(ritz.vectors);  // block restart from the current Ritz vectors
-            ritz.vectors.reset();
+            // block restart from the current Ritz vectors; same width: copy into x so the
+            // captured filter graph (keyed on x's storage) replays instead of recapturing
+            if (ritz.vectors->width == x->width) {
+                CFD_CUDA(cudaMemcpyAsync(x->owned(), ritz.vectors->owned(), x->owned_bytes(),
+                                         cudaMemcpyDeviceToDevice, c.stream));
+            } else {
+                x = std::move(ritz.vectors);
+                ritz.vectors.reset();
+            }
         }
         if (vectors) {
             if (ritz.vectors)
