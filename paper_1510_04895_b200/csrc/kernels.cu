@@ -23,6 +23,9 @@
 #include <cub/device/device_scan.cuh>
 #include <type_traits>
 
+#ifndef CFD_TMA_TR_MIN
+#define CFD_TMA_TR_MIN 64  // minimum rows per TMA tile (whole 32-row chunks); 64: -3.8 % C2 step time vs 32
+#endif
 #ifndef CFD_TMA_MINB
 #define CFD_TMA_MINB 2  // resident CTAs per SM the TMA step kernel is compiled for
 #endif
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(256, CFD_TMA_MINB) step_tma_kernel(const StepP
     const int rr = t / US;
     const int u = t - rr * US;
     const int R = p.R;
-    const int TR = R > 32 ? R : 32;  // rows per tile (whole chunks)
+    const int TR = R > CFD_TMA_TR_MIN ? R : CFD_TMA_TR_MIN;  // rows per tile (whole chunks)
     const int NCH = TR / 32;
     const int cap = MAXW * TR;  // slots per buffer
     int* cols_s = reinterpret_cast<int*>(smem_raw);
@@ -1528,7 +1531,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     for (int u0 = 0; u0 < units; u0 += slab) {
         const int us = std::min(slab, units - u0);
         Geometry g = tma ? geometry_pow2(us) : geometry(us);
-        const int TR = std::max(32, g.R);
+        const int TR = std::max(tma ? CFD_TMA_TR_MIN : 32, g.R);
         const size_t stage = tma ? 2 * static_cast<size_t>(MW) * TR : 0;
         size_t ring = tma ? ((stage * sizeof(int) + 15) & ~size_t(15)) + stage * (CPLX ? 16 : 8)
                           : 0;
