@@ -26,8 +26,11 @@
 #ifndef CFD_TMA_TR_MIN
 #define CFD_TMA_TR_MIN 64  // minimum rows per TMA tile (whole 32-row chunks); 64: -3.8 % C2 step time vs 32
 #endif
+#ifndef CFD_TMA_THREADS
+#define CFD_TMA_THREADS 128  // max threads per CTA of the TMA step kernel
+#endif
 #ifndef CFD_TMA_MINB
-#define CFD_TMA_MINB 2  // resident CTAs per SM the TMA step kernel is compiled for
+#define CFD_TMA_MINB 4  // resident CTAs per SM it is compiled for (128 registers/thread)
 #endif
 
 #include "internal.hpp"
@@ -455,7 +458,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 }
 
 template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
-__global__ void __launch_bounds__(256, CFD_TMA_MINB) step_tma_kernel(const StepParams p) {
+__global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
     constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
@@ -1352,11 +1355,14 @@ const void* find_scaled(const Matrix& a, double s) {
 }
 
 // rows per CTA iteration as a power of two (tiles of whole 32-row chunks)
+// Measured (C2, C3, graphene n_b = 8): small CTAs win -- the per-tile barrier
+// waits on fewer warps -- 128 threads for rows of 8+ units, 64 for narrower.
 inline Geometry geometry_pow2(int units) {
     Geometry g;
     g.US = units;
+    const int cap = units <= 4 ? 64 : CFD_TMA_THREADS;
     int r = 1;
-    while (r * 2 * units <= 256) r *= 2;
+    while (r * 2 * units <= cap) r *= 2;
     g.R = r;
     g.threads = r * units;
     return g;
@@ -1527,7 +1533,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         }
     }
     // column slabs of at most `slab` units (one CTA row-group spans a slab)
-    const int slab = ctx.slab_units > 0 ? std::min(ctx.slab_units, 256) : 256;
+    const int slab_max = tma ? CFD_TMA_THREADS : 256;  // one CTA row-group spans a slab
+    const int slab = ctx.slab_units > 0 ? std::min(ctx.slab_units, slab_max) : slab_max;
     for (int u0 = 0; u0 < units; u0 += slab) {
         const int us = std::min(slab, units - u0);
         Geometry g = tma ? geometry_pow2(us) : geometry(us);
