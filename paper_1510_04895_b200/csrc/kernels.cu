@@ -23,14 +23,11 @@
 #include <cub/device/device_scan.cuh>
 #include <type_traits>
 
-#ifndef CFD_TMA_TR_MIN
-#define CFD_TMA_TR_MIN 64  // minimum rows per TMA tile (whole 32-row chunks); 64: -3.8 % C2 step time vs 32
-#endif
 #ifndef CFD_TMA_THREADS
-#define CFD_TMA_THREADS 128  // max threads per CTA of the TMA step kernel
+#define CFD_TMA_THREADS 256  // max threads per CTA of the TMA step kernel
 #endif
 #ifndef CFD_TMA_MINB
-#define CFD_TMA_MINB 4  // resident CTAs per SM it is compiled for (128 registers/thread)
+#define CFD_TMA_MINB 2  // => 128 registers/thread; CTAs of 64/128 threads then fit 8/4 per SM
 #endif
 
 #include "internal.hpp"
@@ -259,6 +256,7 @@ struct StepParams {
     int nparts;
     int final_launch;
     unsigned* counter;
+    int tr;  // minimum rows per tile of the TMA kernels (32 or 64)
 };
 
 // Sum_j (a_rj * scale) * in[c_rj] over one row, in the row's stored order.
@@ -469,7 +467,7 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
     const int rr = t / US;
     const int u = t - rr * US;
     const int R = p.R;
-    const int TR = R > CFD_TMA_TR_MIN ? R : CFD_TMA_TR_MIN;  // rows per tile (whole chunks)
+    const int TR = R > p.tr ? R : p.tr;  // rows per tile (whole chunks)
     const int NCH = TR / 32;
     const int cap = MAXW * TR;  // slots per buffer
     int* cols_s = reinterpret_cast<int*>(smem_raw);
@@ -1355,12 +1353,22 @@ const void* find_scaled(const Matrix& a, double s) {
 }
 
 // rows per CTA iteration as a power of two (tiles of whole 32-row chunks)
-// Measured (C2, C3, graphene n_b = 8): small CTAs win -- the per-tile barrier
-// waits on fewer warps -- 128 threads for rows of 8+ units, 64 for narrower.
-inline Geometry geometry_pow2(int units) {
+// CTA shape of the TMA kernel, measured on B200 (C1, C2, C3, graphene sweeps):
+// on large operators small CTAs win -- the per-tile barrier waits on fewer
+// warps -- 128 threads and 64-row tiles for rows of 8+ units, 64 threads for
+// narrower rows; operators with fewer than 4 x SMs 64-row tiles (C1) keep
+// 256-thread CTAs and 32-row tiles, or too few CTAs would run.
+struct TmaShape {
+    int cap_threads, tr, slab_max;
+};
+inline TmaShape tma_shape(const Context& ctx, int units, int64_t nrows) {
+    if (nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms)) return {256, 32, 256};
+    if (units <= 4) return {64, 64, 256};
+    return {128, 64, 128};
+}
+inline Geometry geometry_pow2(int units, int cap = CFD_TMA_THREADS) {
     Geometry g;
     g.US = units;
-    const int cap = units <= 4 ? 64 : CFD_TMA_THREADS;
     int r = 1;
     while (r * 2 * units <= cap) r *= 2;
     g.R = r;
@@ -1533,12 +1541,13 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         }
     }
     // column slabs of at most `slab` units (one CTA row-group spans a slab)
-    const int slab_max = tma ? CFD_TMA_THREADS : 256;  // one CTA row-group spans a slab
+    const TmaShape shape = tma_shape(ctx, units, nrows);
+    const int slab_max = tma ? shape.slab_max : 256;  // one CTA row-group spans a slab
     const int slab = ctx.slab_units > 0 ? std::min(ctx.slab_units, slab_max) : slab_max;
     for (int u0 = 0; u0 < units; u0 += slab) {
         const int us = std::min(slab, units - u0);
-        Geometry g = tma ? geometry_pow2(us) : geometry(us);
-        const int TR = std::max(tma ? CFD_TMA_TR_MIN : 32, g.R);
+        Geometry g = tma ? geometry_pow2(us, shape.cap_threads) : geometry(us);
+        const int TR = std::max(tma ? shape.tr : 32, g.R);
         const size_t stage = tma ? 2 * static_cast<size_t>(MW) * TR : 0;
         size_t ring = tma ? ((stage * sizeof(int) + 15) & ~size_t(15)) + stage * (CPLX ? 16 : 8)
                           : 0;
@@ -1552,8 +1561,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
                 cur = smem;
             }
         }
-        static thread_local std::map<std::pair<const void*, int>, int> occ_cache;
-        auto key = std::make_pair(reinterpret_cast<const void*>(kernel), g.threads);
+        static thread_local std::map<std::tuple<const void*, int, size_t>, int> occ_cache;
+        auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), g.threads, smem);
         auto it = occ_cache.find(key);
         int maxb = 0;
         if (it == occ_cache.end()) {
@@ -1603,6 +1612,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         p.nparts = s.partial_base + grid;
         p.final_launch = s.final_launch ? 1 : 0;
         p.counter = ctx.counter.as<unsigned>();
+        p.tr = TR;
         if (nrows > 0) {
             kernel<<<grid, g.threads, smem, st>>>(p);
             CFD_CUDA(cudaGetLastError());

@@ -320,3 +320,30 @@ def test_staged_kernel_bitexact(ctx, orc, name, l, nb, boundary, kernel):
         assert np.allclose(d, dref, rtol=1e-12, atol=1e-12 * np.max(np.abs(dref)))
     finally:
         ctx.set_option("kernel", "tma")
+
+
+@pytest.mark.parametrize("name,l,nb", [("ti", (24, 24, 17), 32), ("ti", (24, 24, 17), 7),
+                                       ("graphene", (160, 128), 4), ("graphene", (160, 128), 1),
+                                       ("graphene", (160, 128), 9)])
+def test_large_operator_cta_shapes_bitexact(ctx, orc, name, l, nb):
+    """Operators above 4 x SMs 64-row tiles take the large-problem CTA shapes
+    (128-thread CTAs with 64-row tiles; 64-thread CTAs for rows of <= 4 units)
+    -- fused W/X bit-exact with dots, apply_filter X bit-exact with moments."""
+    A, c = make_case(ctx, orc, name, l)
+    assert c.dim // 64 >= 4 * 148
+    cx = name == "ti"
+    u, w, x = (orc.randomize(c.dim, nb, s, cx) for s in (1, 2, 3))
+    U, W, X = block(A, u), block(A, w), block(A, x)
+    bounds = (-5.6, 5.6) if cx else (-3.2, 3.3)
+    p = cf.make_filter((-0.2, 0.3), bounds, 6, "lanczos2")
+    cf.apply_filter(A, block(A, x), p)  # creates the pre-scaled values the TMA path uses
+    d = cf.spmmvm_fused(A, U, W, X, p.alpha, p.beta, 0.83, dots=True)
+    dref = orc.spmmvm_fused(c, u, w, x, p.alpha, p.beta, 0.83, want_dots=True)
+    assert bits_equal(W.to_numpy(), w) and bits_equal(X.to_numpy(), x)
+    assert np.allclose(d, dref, rtol=1e-12, atol=1e-12 * np.max(np.abs(dref)))
+    x0 = orc.randomize(c.dim, nb, 9, cx)
+    Xf = block(A, x0)
+    mom = cf.apply_filter(A, Xf, p, want_moments=True)
+    xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+    assert bits_equal(Xf.to_numpy(), xr)
+    assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
