@@ -77,7 +77,10 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count);
 /* Options: CHEBFD_OPT_GRAPHS (1 = capture apply_filter into cached CUDA
  * graphs, default 1); CHEBFD_OPT_OVERLAP (1 = overlap the halo exchange with
  * interior rows, default 1); CHEBFD_OPT_KERNEL (step kernel variant: 0 plain
- * register gathers, 1 TMA-staged SELL chunks with pre-scaled values; default 1). */
+ * register gathers; 1 TMA-staged SELL chunks with pre-scaled values, and the
+ * two-units-per-thread kernel for rows of <= 8 entries -- default; 2 also the
+ * gathered rows staged in shared memory (experimental); 3 the two-units kernel
+ * wherever it applies).  All variants give bit-identical rows. */
 /* CHEBFD_OPT_SLAB_UNITS (step kernels sweep the block in column slabs of at
  * most this many 16-byte units; 0 = 256, the measured best -- narrower slabs
  * re-read the matrix per slab).  Changing any option drops captured filters. */

@@ -422,8 +422,6 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
     HostCsr csr = ti ? gen_topological_insulator(s, r0, r1) : gen_graphene(s, r0, r1);
     const int64_t nnz_g = allreduce_count(c, static_cast<int64_t>(csr.cols.size()));
     auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g);
-    m->plane_rows = ti ? 4 * s.lx * s.ly : 2 * s.lx;
-    m->line_rows = ti ? 4 * s.lx : 0;
     return m;
 }
 

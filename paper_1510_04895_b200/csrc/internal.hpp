@@ -96,8 +96,6 @@ struct Matrix {
     int kind = 0;
     int64_t nnz_global = 0, nnz_local = 0;
     int max_row_len = 0;
-    int64_t plane_rows = 0;  // lattice plane (TI z-plane, graphene y-row); 0 = unknown
-    int64_t line_rows = 0;   // one lattice line inside a plane (TI y-row of sites)
     Partition part;
     int64_t nchunks = 0;
     int64_t entries = 0;     // SELL slots (padding included)
