@@ -192,15 +192,38 @@ def run_ours(args):
     e_steps = max(1, min(args.steps, 5))
     for _ in range(e_steps):
         cf.apply_filter_host(A, xc, p)
-    e2e_s = (time.perf_counter() - t0) / e_steps
+    sync_s = (time.perf_counter() - t0) / e_steps
+    # streamed: the same per-step host->device / device->host copies through
+    # chebfd_filter_pipe, overlapped with the neighbouring steps' filters
+    xb = cf.host_array((D, nb), np.complex128)
+    xb[:] = xc
+    bufs = (xc, xb)
+    pipe = cf.FilterPipe(A, nb)
+    for k in range(2):
+        pipe.submit(bufs[k % 2], p)
+    pipe.wait()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        pipe.submit(bufs[k % 2], p)
+    pipe.wait()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    pipe.close()
     if dist:
         import torch
-        t = torch.tensor([e2e_s], dtype=torch.float64)
+        t = torch.tensor([e2e_s, sync_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
+        e2e_s, sync_s = float(t[0]), float(t[1])
+    del xb, bufs
     lib.chebfd_host_free(host)
     e2e = dict(value=total_flops / e2e_s / 1e9, unit=UNIT, h2d_bytes_per_step=nbytes,
-               d2h_bytes_per_step=nbytes, ms_per_step=e2e_s * 1e3, steps=e2e_steps_note(e_steps))
+               d2h_bytes_per_step=nbytes, ms_per_step=e2e_s * 1e3, steps=args.steps,
+               mode="streamed: chebfd_filter_pipe, pinned host blocks, every step's H2D input "
+                    "copy and D2H result copy inside the timed region, overlapped with the "
+                    "neighbouring steps' filters",
+               sync_value=total_flops / sync_s / 1e9, sync_ms_per_step=sync_s * 1e3,
+               sync_steps=e2e_steps_note(e_steps))
     out = None
     if rank == 0:
         out = {

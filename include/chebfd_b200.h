@@ -84,8 +84,19 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count);
 /* CHEBFD_OPT_SLAB_UNITS (step kernels sweep the block in column slabs of at
  * most this many 16-byte units; 0 = 256, the measured best -- narrower slabs
  * re-read the matrix per slab).  Changing any option drops captured filters. */
+/* CHEBFD_OPT_PAIR (default 0): apply_filter runs two fused steps per launch as a
+ * wavefront over the rows that keeps the intermediate vector in L2 (0 off;
+ * 1 where the whole filter state is L2-resident; 2 wherever it applies:
+ * single-rank operators, rows of <= 16 entries, rows of <= 256 16-byte units).
+ * Bit-identical to two single steps.  CHEBFD_OPT_PAIR_TILE_ROWS / _THREADS /
+ * _EXTRA tune its tile rows, CTA threads and extra lag tiles (0/0/-1: auto);
+ * CHEBFD_OPT_PAIR_HINTS (default 1) sets its L2 eviction-priority hints;
+ * CHEBFD_OPT_PAIR_SLAB its column-slab width in 16-byte units (0: the widest
+ * slab whose wavefront fits the L2). */
 enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
-       CHEBFD_OPT_SLAB_UNITS = 5 };
+       CHEBFD_OPT_SLAB_UNITS = 5, CHEBFD_OPT_PAIR = 6, CHEBFD_OPT_PAIR_TILE_ROWS = 7,
+       CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
+       CHEBFD_OPT_PAIR_SLAB = 11 };
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */
@@ -272,6 +283,22 @@ int chebfd_apply_filter(chebfd_matrix* a, chebfd_block* x, const double* combine
 int chebfd_apply_filter_host(chebfd_matrix* a, void* x_host, int64_t width,
                              const double* combined, int degree, double alpha, double beta,
                              double* moments);
+
+/* Streamed end-to-end filtering of a sequence of HOST blocks (no reference
+ * counterpart: the reference filters in place in host memory).  Job k's
+ * H2D copy runs on its own stream while job k-1 filters and job k-2's result
+ * copies back, so a stream of filter applications runs at the device rate,
+ * not at device + PCIe time.  Two device slots of nb columns; submit() returns
+ * once the work is queued: host_in must stay valid until its H2D copy ran and
+ * host_out until wait() (pinned memory from chebfd_host_alloc for full-speed
+ * copies; host_in == host_out is allowed).  Results are bit-identical to
+ * chebfd_apply_filter_host. */
+typedef struct chebfd_filter_pipe chebfd_filter_pipe;
+int chebfd_filter_pipe_create(chebfd_matrix* a, int64_t width, chebfd_filter_pipe** out);
+int chebfd_filter_pipe_submit(chebfd_filter_pipe* p, const void* host_in, void* host_out,
+                              const double* combined, int degree, double alpha, double beta);
+int chebfd_filter_pipe_wait(chebfd_filter_pipe* p);
+int chebfd_filter_pipe_destroy(chebfd_filter_pipe* p);
 
 /* ---- solver (solver.hpp / solver.cpp) ------------------------------------------- */
 /* SVQB (solver.cpp:32-61): q receives the rank orthonormal columns first. */

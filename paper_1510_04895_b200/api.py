@@ -155,8 +155,12 @@ class Context:
 
     def set_option(self, name: str, value):
         """graphs (bool), overlap (bool), kernel ("gather" | "tma"),
-        slab_units (int, 0 = 256)."""
-        code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5}[name]
+        slab_units (int, 0 = 256), pair (0 off | 1 auto | 2 force: two fused
+        steps per wavefront launch), pair_tile_rows / pair_threads /
+        pair_extra (pair-kernel tuning, 0 / 0 / -1 = automatic)."""
+        code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5, "pair": 6,
+                "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
+                "pair_slab": 11}[name]
         if name == "kernel" and isinstance(value, str):
             value = {"gather": 0, "tma": 1, "stage": 2, "tma2": 3}[value]
         _check(_lib().chebfd_ctx_set_option(self._h, code, int(value)))
@@ -593,6 +597,52 @@ def apply_filter_host(A: SparseMatrix, x: np.ndarray, p: FilterPolynomial,
     _check(_lib().chebfd_apply_filter_host(A._h, _ptr(x), x.shape[1], _ptr(comb), p.degree,
                                            p.alpha, p.beta, _ptr(mom)))
     return MomentTable(p.degree, x.shape[1], mom) if want_moments else None
+
+
+class FilterPipe:
+    """Streamed end-to-end filtering of host blocks (chebfd_filter_pipe_*): the
+    H2D copy of job k and the D2H copy of job k-2 overlap the filter of job k-1.
+    Host arrays must stay alive until wait(); pinned ones (host_array) copy at
+    full PCIe speed."""
+
+    def __init__(self, A: SparseMatrix, width: int):
+        self.A = A
+        self.width_ = int(width)
+        self._h = C.c_void_p()
+        _check(_lib().chebfd_filter_pipe_create(A._h, self.width_, C.byref(self._h)))
+        self._keep = []
+
+    def submit(self, x_in: np.ndarray, p: "FilterPolynomial", x_out: Optional[np.ndarray] = None):
+        x_out = x_in if x_out is None else x_out
+        for x in (x_in, x_out):
+            if x.dtype != self.A.dtype or not x.flags.c_contiguous or x.shape != (self.A.local_rows, self.width_):
+                raise InvalidArgument("filter_pipe: host block must be C-contiguous "
+                                      "(local rows x width) of the matrix dtype")
+        comb = np.ascontiguousarray(p.combined, dtype=np.float64)
+        self._keep.append((x_in, x_out))
+        _check(_lib().chebfd_filter_pipe_submit(self._h, _ptr(x_in), _ptr(x_out), _ptr(comb),
+                                                p.degree, p.alpha, p.beta))
+
+    def wait(self):
+        _check(_lib().chebfd_filter_pipe_wait(self._h))
+        self._keep.clear()
+
+    def close(self):
+        if self._h:
+            _check(_lib().chebfd_filter_pipe_destroy(self._h))
+            self._h = None
+
+
+def host_array(shape, dtype):
+    """A numpy array over pinned host memory (chebfd_host_alloc); freed with the array."""
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    ptr = C.c_void_p()
+    _check(_lib().chebfd_host_alloc(max(nbytes, 1), C.byref(ptr)))
+    buf = (C.c_char * max(nbytes, 1)).from_address(ptr.value)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+    weakref.finalize(buf, _lib().chebfd_host_free, C.c_void_p(ptr.value))
+    return arr
 
 
 # ------------------------------------------------------------------ solver --

@@ -426,6 +426,33 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
 }
 
 // --------------------------------------------------------- apply_filter --
+// Fused steps n and n+1 in one wavefront launch where it applies (pair.cu):
+// single-rank operators (no halo exchange between the steps), no dots.
+bool run_pair_step(Context& c, const Matrix& a, Block& u, Block& w, Block& x, double alpha,
+                   double beta, const double* coeff_dev, int n, void* x0, double* mom) {
+    if (c.pair_mode == 0 || c.kernel_variant < 1) return false;
+    if (a.part.halo_lo != 0 || a.part.halo_hi != 0) return false;
+    StepArgs s{};
+    s.kind_step = kStepFused;
+    s.a = &a;
+    s.width_cols = u.width;
+    s.in = gather_base(a, u);
+    s.w = w.owned();
+    s.x = x.owned();
+    s.x0 = x0;
+    s.alpha = 2.0 * alpha;
+    s.beta = 2.0 * beta;
+    s.coeff_dev = coeff_dev;
+    s.coeff_index = n;
+    s.dots_mode = mom ? 2 : 0;
+    s.dots_out = mom;
+    s.row0 = 0;
+    s.row1 = a.part.local;
+    s.partial_base = 0;
+    s.final_launch = true;
+    return launch_step_pair(c, s, c.stream);
+}
+
 FilterWorkspace& filter_workspace(Context& c, const Matrix& a, int64_t width, bool moments) {
     auto key = std::make_tuple(static_cast<const void*>(&a), width, a.kind);
     FilterWorkspace& ws = c.filter_ws[key];
@@ -466,6 +493,14 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     Block* pw = ws.w.get();
     for (int n = 3; n <= degree; ++n) {
         std::swap(pu, pw);  // swap handles, never copies
+        if (n < degree && run_pair_step(c, a, *pu, *pw, x, alpha, beta, coeff_dev, n,
+                                        moments ? ws.x0->owned() : nullptr,
+                                        moments ? mom_dev + static_cast<int64_t>(n) * nb : nullptr)) {
+            // steps n and n+1 done: W holds V_n, U holds V_{n+1} -- the roles after step n+1
+            std::swap(pu, pw);
+            ++n;
+            continue;
+        }
         StepArgs f{};
         f.kind_step = kStepFused;
         f.w = pw->owned();
@@ -693,6 +728,18 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->kernel_variant = static_cast<int>(value);
         else if (option == CHEBFD_OPT_SLAB_UNITS)
             c->slab_units = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PAIR)
+            c->pair_mode = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
+            c->pair_tile_rows = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PAIR_THREADS)
+            c->pair_threads = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PAIR_EXTRA)
+            c->pair_extra = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PAIR_HINTS)
+            c->pair_hints = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PAIR_SLAB)
+            c->pair_slab = static_cast<int>(value);
         else
             fail(CHEBFD_ERR_INVALID_ARGUMENT, "unknown option");
     });
@@ -1148,6 +1195,89 @@ int chebfd_apply_filter_host(chebfd_matrix* a, void* x_host, int64_t width, cons
                                  c.stream));
         ctx_sync(c);
     });
+}
+
+// ---- streamed host filtering ------------------------------------------------------
+struct FilterPipe {
+    Context* c = nullptr;
+    Matrix* m = nullptr;
+    int64_t width = 0;
+    std::unique_ptr<Block> slot[2];
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t in_ready[2] = {}, done[2] = {}, out_done[2] = {};
+    bool used[2] = {false, false};
+    int next = 0;
+    ~FilterPipe() {
+        if (h2d) cudaStreamSynchronize(h2d);
+        if (d2h) cudaStreamSynchronize(d2h);
+        if (c) cudaStreamSynchronize(c->stream);
+        for (int i = 0; i < 2; ++i) {
+            if (in_ready[i]) cudaEventDestroy(in_ready[i]);
+            if (done[i]) cudaEventDestroy(done[i]);
+            if (out_done[i]) cudaEventDestroy(out_done[i]);
+        }
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
+    }
+};
+
+int chebfd_filter_pipe_create(chebfd_matrix* a, int64_t width, chebfd_filter_pipe** out) {
+    return guard([&] {
+        require(a != nullptr && out != nullptr, "filter_pipe_create: null argument");
+        require(width >= 1, "filter_pipe_create: width must be >= 1");
+        Matrix& m = *reinterpret_cast<Matrix*>(a);
+        auto p = std::make_unique<FilterPipe>();
+        p->c = m.ctx;
+        p->m = &m;
+        p->width = width;
+        for (int i = 0; i < 2; ++i) {
+            p->slot[i] = make_block(*m.ctx, &m, m.kind, m.part.local, width);
+            CFD_CUDA(cudaEventCreateWithFlags(&p->in_ready[i], cudaEventDisableTiming));
+            CFD_CUDA(cudaEventCreateWithFlags(&p->done[i], cudaEventDisableTiming));
+            CFD_CUDA(cudaEventCreateWithFlags(&p->out_done[i], cudaEventDisableTiming));
+        }
+        CFD_CUDA(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
+        CFD_CUDA(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+        *out = reinterpret_cast<chebfd_filter_pipe*>(p.release());
+    });
+}
+
+int chebfd_filter_pipe_submit(chebfd_filter_pipe* pipe, const void* host_in, void* host_out,
+                              const double* combined, int degree, double alpha, double beta) {
+    return guard([&] {
+        require(pipe != nullptr && host_in != nullptr && host_out != nullptr,
+                "filter_pipe_submit: null argument");
+        FilterPipe& p = *reinterpret_cast<FilterPipe*>(pipe);
+        if (degree < 2) fail(CHEBFD_ERR_INVALID_ARGUMENT, "apply_filter: degree must be >= 2");
+        Context& c = *p.c;
+        const int s = p.next;
+        p.next ^= 1;
+        Block& X = *p.slot[s];
+        // the slot's previous result must have left before new input lands in it
+        if (p.used[s]) CFD_CUDA(cudaStreamWaitEvent(p.h2d, p.out_done[s], 0));
+        CFD_CUDA(cudaMemcpyAsync(X.owned(), host_in, X.owned_bytes(), cudaMemcpyHostToDevice, p.h2d));
+        CFD_CUDA(cudaEventRecord(p.in_ready[s], p.h2d));
+        CFD_CUDA(cudaStreamWaitEvent(c.stream, p.in_ready[s], 0));
+        apply_filter_device(c, *p.m, X, combined, degree, alpha, beta, nullptr);
+        CFD_CUDA(cudaEventRecord(p.done[s], c.stream));
+        CFD_CUDA(cudaStreamWaitEvent(p.d2h, p.done[s], 0));
+        CFD_CUDA(cudaMemcpyAsync(host_out, X.owned(), X.owned_bytes(), cudaMemcpyDeviceToHost, p.d2h));
+        CFD_CUDA(cudaEventRecord(p.out_done[s], p.d2h));
+        p.used[s] = true;
+    });
+}
+
+int chebfd_filter_pipe_wait(chebfd_filter_pipe* pipe) {
+    return guard([&] {
+        require(pipe != nullptr, "filter_pipe_wait: null pipe");
+        FilterPipe& p = *reinterpret_cast<FilterPipe*>(pipe);
+        CFD_CUDA(cudaStreamSynchronize(p.d2h));
+        CFD_CUDA(cudaStreamSynchronize(p.c->stream));
+    });
+}
+
+int chebfd_filter_pipe_destroy(chebfd_filter_pipe* pipe) {
+    return guard([&] { delete reinterpret_cast<FilterPipe*>(pipe); });
 }
 
 }  // extern "C"

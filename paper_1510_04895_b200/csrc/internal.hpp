@@ -115,6 +115,8 @@ struct Matrix {
     // and 2 alpha); at most 4 are kept
     std::vector<std::pair<double, std::unique_ptr<DeviceBuffer>>> scaled;
     bool scaled_evicted = false;
+    int64_t band = 0;       // max |extended column - extended row| over all entries
+    DeviceBuffer pair_sync; // pair kernel: item / exit tickets + per-1024-row group counters (zeroed)
 };
 
 // ---- block vector -------------------------------------------------------------------
@@ -178,6 +180,10 @@ struct Context {
                              // 2 TMA-staged matrix chunks + gathered rows (where a plan fits)
     int64_t launches = 0;
     int slab_units = 0;   // step kernel column-slab width in 16-byte units (0: up to 256)
+    // two fused steps per launch (pair.cu): 0 off, 1 where the wavefront's working set
+    // fits the L2, 2 wherever the kernel applies; tuning knobs (0 / -1: automatic)
+    int pair_mode = 0, pair_tile_rows = 0, pair_threads = 0, pair_extra = -1, pair_hints = 1,
+        pair_slab = 0;
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
     DeviceBuffer partials;   // per-block partial sums
     DeviceBuffer counter;    // last-block-done ticket (uint32), self-resetting
@@ -231,6 +237,10 @@ struct StepArgs {
     int* grid_used;          // out: number of blocks used
 };
 void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st);
+// Steps coeff_index and coeff_index+1 of apply_filter's fused loop in one
+// wavefront launch (pair.cu); s.in = U, s.w = W as for the first step.
+// Returns false (nothing launched) where the pair kernel does not apply.
+bool launch_step_pair(Context& ctx, const StepArgs& s, cudaStream_t st);
 
 // cache a copy of a's values multiplied by s (used by the v3 step kernel)
 void ensure_scaled_values(Context& ctx, Matrix& a, double s, cudaStream_t st);

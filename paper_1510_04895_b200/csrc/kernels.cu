@@ -31,317 +31,11 @@
 #endif
 
 #include "internal.hpp"
+#include "step_common.cuh"
 
 namespace cfd {
 
 namespace {
-
-__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
-
-template <class T>
-__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
-
-// Streaming loads/stores (evict-first) for the read-once / write-once streams.
-__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
-__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
-__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
-__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
-
-// ---- scalar traits: (complex?, unit type) ------------------------------------------
-template <bool CPLX, class T>
-struct Ops;
-
-// real, one column per unit
-template <>
-struct Ops<false, double> {
-    using M = double;
-    static constexpr int kCols = 1;
-    __device__ static double zero() { return 0.0; }
-    __device__ static M scale(M a, double s) { return mul(a, s); }
-    __device__ static double prod(M a, double u) { return mul(a, u); }
-    __device__ static double vadd(double a, double b) { return add(a, b); }
-    __device__ static double vsub(double a, double b) { return sub(a, b); }
-    __device__ static double smul(double s, double v) { return mul(s, v); }
-    __device__ static double cdot(double x, double w) { return mul(x, w); }
-    __device__ static double lam_mul(const double* lam, int col, double v) { return mul(lam[col], v); }
-    __device__ static double cdiv(double v, const double* d, int col) { return div_(v, d[col]); }
-    __device__ static void store_re(double* out, int unit, double v) { out[unit] = v; }
-    __device__ static void store_full(double* out, int unit, double v) { out[unit] = v; }
-};
-
-// real, two columns per unit
-template <>
-struct Ops<false, double2> {
-    using M = double;
-    static constexpr int kCols = 2;
-    __device__ static double2 zero() { return make_double2(0.0, 0.0); }
-    __device__ static M scale(M a, double s) { return mul(a, s); }
-    __device__ static double2 prod(M a, double2 u) { return make_double2(mul(a, u.x), mul(a, u.y)); }
-    __device__ static double2 vadd(double2 a, double2 b) { return make_double2(add(a.x, b.x), add(a.y, b.y)); }
-    __device__ static double2 vsub(double2 a, double2 b) { return make_double2(sub(a.x, b.x), sub(a.y, b.y)); }
-    __device__ static double2 smul(double s, double2 v) { return make_double2(mul(s, v.x), mul(s, v.y)); }
-    __device__ static double2 cdot(double2 x, double2 w) { return make_double2(mul(x.x, w.x), mul(x.y, w.y)); }
-    __device__ static double2 lam_mul(const double* lam, int col, double2 v) {
-        return make_double2(mul(lam[col], v.x), mul(lam[col + 1], v.y));
-    }
-    __device__ static double2 cdiv(double2 v, const double* d, int col) {
-        return make_double2(div_(v.x, d[col]), div_(v.y, d[col + 1]));
-    }
-    __device__ static void store_re(double* out, int unit, double2 v) {
-        out[2 * unit] = v.x;
-        out[2 * unit + 1] = v.y;
-    }
-    __device__ static void store_full(double2* out, int unit, double2 v) { out[unit] = v; }
-};
-
-// complex, one column per unit (std::complex<double> layout)
-template <>
-struct Ops<true, double2> {
-    using M = double2;
-    static constexpr int kCols = 1;
-    __device__ static double2 zero() { return make_double2(0.0, 0.0); }
-    // complex * double (libstdc++ operator*(complex, T): componentwise)
-    __device__ static M scale(M a, double s) { return make_double2(mul(a.x, s), mul(a.y, s)); }
-    // complex * complex, GCC inline expansion: (ac - bd, ad + bc)
-    __device__ static double2 prod(M a, double2 u) {
-        return make_double2(sub(mul(a.x, u.x), mul(a.y, u.y)), add(mul(a.x, u.y), mul(a.y, u.x)));
-    }
-    __device__ static double2 vadd(double2 a, double2 b) { return make_double2(add(a.x, b.x), add(a.y, b.y)); }
-    __device__ static double2 vsub(double2 a, double2 b) { return make_double2(sub(a.x, b.x), sub(a.y, b.y)); }
-    __device__ static double2 smul(double s, double2 v) { return make_double2(mul(s, v.x), mul(s, v.y)); }
-    // conj(x) * w
-    __device__ static double2 cdot(double2 x, double2 w) {
-        const double nxi = -x.y;
-        return make_double2(sub(mul(x.x, w.x), mul(nxi, w.y)), add(mul(x.x, w.y), mul(nxi, w.x)));
-    }
-    __device__ static double2 lam_mul(const double* lam, int col, double2 v) { return smul(lam[col], v); }
-    __device__ static double2 cdiv(double2 v, const double* d, int col) {
-        return make_double2(div_(v.x, d[col]), div_(v.y, d[col]));
-    }
-    __device__ static void store_re(double* out, int unit, double2 v) { out[unit] = v.x; }
-    __device__ static void store_full(double2* out, int unit, double2 v) { out[unit] = v; }
-};
-
-template <class T>
-__device__ __forceinline__ void kahan_add(T& s, T& c, T v);
-template <>
-__device__ __forceinline__ void kahan_add<double>(double& s, double& c, double v) {
-    const double y = sub(v, c);
-    const double t = add(s, y);
-    c = sub(sub(t, s), y);
-    s = t;
-}
-template <>
-__device__ __forceinline__ void kahan_add<double2>(double2& s, double2& c, double2 v) {
-    kahan_add<double>(s.x, c.x, v.x);
-    kahan_add<double>(s.y, c.y, v.y);
-}
-
-template <class T>
-__device__ __forceinline__ T tadd(T a, T b);
-template <>
-__device__ __forceinline__ double tadd<double>(double a, double b) { return add(a, b); }
-template <>
-__device__ __forceinline__ double2 tadd<double2>(double2 a, double2 b) {
-    return make_double2(add(a.x, b.x), add(a.y, b.y));
-}
-
-// L2-coherent load of a partial (double, double2, or a pair of double2 units)
-template <class T>
-__device__ __forceinline__ T ldcg_t(const T* p) {
-    if constexpr (std::is_same_v<T, double> || std::is_same_v<T, double2>) {
-        return __ldcg(p);
-    } else {
-        const double2* q = reinterpret_cast<const double2*>(p);
-        return T{__ldcg(q), __ldcg(q + 1)};
-    }
-}
-
-// ---- fixed-order block + grid reduction of NDOT per-unit accumulators -------------
-// Threads are laid out t = rr*US + u.  Each CTA writes NDOT*US partials; the
-// last CTA to finish (ticket) sums partial rows [0, nparts) in order and
-// hands the totals to `emit(d, u, value)`.
-template <class T, int NDOT, class Emit>
-__device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1], int R, int US,
-                                            T* partials, int part_slot, int nparts, bool final_launch,
-                                            unsigned* counter, Emit emit) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* sred = reinterpret_cast<T*>(smem_raw);
-    const int t = threadIdx.x;
-    const int rr = t / US, u = t - rr * US;
-    const int nthr = R * US;
-#pragma unroll
-    for (int d = 0; d < NDOT; ++d) sred[d * nthr + t] = acc[d];
-    __syncthreads();
-    if (rr == 0) {
-#pragma unroll
-        for (int d = 0; d < NDOT; ++d) {
-            T s = sred[d * nthr + u];
-            for (int q = 1; q < R; ++q) s = tadd(s, sred[d * nthr + q * US + u]);
-            partials[(static_cast<int64_t>(part_slot) * NDOT + d) * US + u] = s;
-        }
-    }
-    if (!final_launch) return;
-    __threadfence();
-    __syncthreads();
-    __shared__ unsigned is_last;
-    if (t == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-#pragma unroll
-    for (int d = 0; d < NDOT; ++d) {
-        // partials rr, rr + R, rr + 2R, ... summed left to right; eight loads in
-        // flight per step (the order, hence every bit, is the sequential loop's)
-        auto at = [&](int q) {
-            return ldcg_t(&partials[(static_cast<int64_t>(q) * NDOT + d) * US + u]);
-        };
-        T s = T{};
-        int q = rr;
-        if (q < nparts) {
-            s = at(q);
-            q += R;
-        }
-        for (; q + 7 * R < nparts; q += 8 * R) {
-            T v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = at(q + k * R);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) s = tadd(s, v[k]);
-        }
-        for (; q < nparts; q += R) s = tadd(s, at(q));
-        sred[d * nthr + t] = s;
-    }
-    __syncthreads();
-    if (rr == 0) {
-#pragma unroll
-        for (int d = 0; d < NDOT; ++d) {
-            T s = sred[d * nthr + u];
-            const int lim = R < nparts ? R : nparts;
-            for (int q = 1; q < lim; ++q) s = tadd(s, sred[d * nthr + q * US + u]);
-            emit(d, u, s);
-        }
-    }
-    if (t == 0) *counter = 0u;  // self-reset for the next stream-ordered launch
-}
-
-// ---- the Chebyshev step kernel --------------------------------------------------------
-struct StepParams {
-    const int64_t* chunk_ptr;
-    const unsigned char* chunk_full;  // 1: every row of the chunk has exactly `width` entries
-    const int* cols;
-    const void* vals;
-    const void* svals;    // values pre-multiplied by `alpha` (or null)
-    int64_t row0, row1;   // owned rows of this launch
-    int64_t halo_lo;      // extended-row offset of owned row 0
-    int pitch;            // units per row in memory
-    int u_off;            // first unit of this column slab
-    int US;               // units in this slab (threads per row)
-    int R;                // rows per CTA iteration
-    const void* in;       // gathered operand (extended base)
-    void* w;              // owned base
-    void* x;
-    void* x0;
-    double alpha, beta;   // already 2x for start2/fused/recur
-    double c0, c1, c2;
-    const double* coeff_dev;
-    int coeff_index;
-    void* dots_out;
-    int64_t dots_row_stride;  // doubles between the NDOT output rows (moment rows)
-    void* partials;
-    int part_base;
-    int nparts;
-    int final_launch;
-    unsigned* counter;
-    int tr;  // minimum rows per tile of the TMA kernels (32 or 64)
-};
-
-// Sum_j (a_rj * scale) * in[c_rj] over one row, in the row's stored order.
-// MAXW > 0: all column indices of the row are loaded first, then every
-// gather is issued before the first use (maximum memory-level parallelism).
-template <class O, class T, class M, int MAXW>
-__device__ __forceinline__ T gather_row(const int* __restrict__ cols, const M* __restrict__ vals,
-                                        const T* __restrict__ in, int64_t base, int width, int lane,
-                                        int pitch, int64_t col_off, double scale) {
-    T acc = O::zero();
-    if constexpr (MAXW > 0) {
-        int c[MAXW];
-#pragma unroll
-        for (int j = 0; j < MAXW; ++j)
-            c[j] = (j < width) ? __ldg(&cols[base + static_cast<int64_t>(j) * 32 + lane]) : -1;
-        T g[MAXW];
-#pragma unroll
-        for (int j = 0; j < MAXW; ++j)
-            if (c[j] >= 0) g[j] = ldg(&in[static_cast<int64_t>(c[j]) * pitch + col_off]);
-#pragma unroll
-        for (int j = 0; j < MAXW; ++j)
-            if (c[j] >= 0) {
-                const M v = __ldg(&vals[base + static_cast<int64_t>(j) * 32 + lane]);
-                acc = O::vadd(acc, O::prod(O::scale(v, scale), g[j]));
-            }
-    } else {
-        constexpr int BATCH = 8;
-        for (int j0 = 0; j0 < width; j0 += BATCH) {
-            int c[BATCH];
-            T g[BATCH];
-#pragma unroll
-            for (int b = 0; b < BATCH; ++b)
-                c[b] = (j0 + b < width) ? __ldg(&cols[base + static_cast<int64_t>(j0 + b) * 32 + lane]) : -1;
-#pragma unroll
-            for (int b = 0; b < BATCH; ++b)
-                if (c[b] >= 0) g[b] = ldg(&in[static_cast<int64_t>(c[b]) * pitch + col_off]);
-#pragma unroll
-            for (int b = 0; b < BATCH; ++b)
-                if (c[b] >= 0) {
-                    const M v = __ldg(&vals[base + static_cast<int64_t>(j0 + b) * 32 + lane]);
-                    acc = O::vadd(acc, O::prod(O::scale(v, scale), g[b]));
-                }
-        }
-    }
-    return acc;
-}
-
-// Per-entry epilogue of each step kind, in the reference's operation order.
-template <class O, class T, int KIND, int DMODE, int NA>
-__device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T wi, const T xi,
-                                              const T x0v, int64_t own, T* __restrict__ W,
-                                              T* __restrict__ X, T* __restrict__ X0, double beta,
-                                              double coeff, double c1, double c2, T (&acc_d)[NA],
-                                              T (&comp_d)[NA]) {
-    if constexpr (KIND == kStepSpmmvm) {
-        T y = acc;
-        if (beta != 0.0) y = O::vadd(y, O::smul(beta, ui));  // kernels.hpp:62-65
-        st_stream(&W[own], y);
-        if constexpr (DMODE == 3) {  // apply_filter entry: x0 = X, m0 = <x,x>, m1 = <x,u>
-            st_stream(&X0[own], ui);
-            acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, ui));
-            acc_d[1] = O::vadd(acc_d[1], O::cdot(ui, y));
-        }
-    } else if constexpr (KIND == kStepStart2) {
-        // w = spmmvm(A,u,2a,2b); w = 1*w + (-1)*x + 0*x; x = c0 x + c1 u + c2 w  (filter.hpp:93-103)
-        T wr = acc;
-        if (beta != 0.0) wr = O::vadd(wr, O::smul(beta, ui));
-        const T wn = O::vadd(O::vadd(O::smul(1.0, wr), O::smul(-1.0, xi)), O::smul(0.0, xi));
-        st_stream(&W[own], wn);
-        if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(xi, wn));
-        const T xn = O::vadd(O::vadd(O::smul(coeff, xi), O::smul(c1, ui)), O::smul(c2, wn));
-        st_stream(&X[own], xn);
-    } else {
-        // fused / recur: w' = tmp + 2b u_i - w_i  (kernels.hpp:103,142)
-        const T wn = O::vsub(O::vadd(acc, O::smul(beta, ui)), wi);
-        st_stream(&W[own], wn);
-        if constexpr (KIND == kStepFused) {
-            if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
-            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
-            st_stream(&X[own], O::vadd(xi, O::smul(coeff, wn)));  // kernels.hpp:106
-        } else {
-            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
-        }
-    }
-}
 
 template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 __global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
@@ -425,35 +119,6 @@ __global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
 // read indices/values from shared memory, so registers only hold the
 // gathered neighbour units in flight.  Own-row streams (W, X, x0) are plain
 // coalesced loads issued ahead of the gathers.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "LAB_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra LAB_WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
 
 template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel(const StepParams p) {
@@ -1308,7 +973,8 @@ template <class M>
 __global__ void sell_fill_kernel(const int64_t* __restrict__ offs, const int64_t* __restrict__ gcols,
                                  const M* __restrict__ gvals, int64_t rows,
                                  const int64_t* __restrict__ chunk_ptr, int* __restrict__ cols,
-                                 M* __restrict__ vals, ColMap cm, int* __restrict__ err) {
+                                 M* __restrict__ vals, ColMap cm, int* __restrict__ err,
+                                 unsigned long long* __restrict__ band) {
     const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t nch = (rows + kChunk - 1) / kChunk;
     if (r >= nch * kChunk) return;
@@ -1317,11 +983,14 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ offs, const int64_t
     const int64_t base = chunk_ptr[chunk];
     const int64_t width = (chunk_ptr[chunk + 1] - base) / kChunk;
     const int64_t b = r < rows ? offs[r] : 0, e = r < rows ? offs[r + 1] : 0;
+    int64_t dist = 0;
     for (int64_t j = 0; j < width; ++j) {
         const int64_t slot = base + j * kChunk + lane;
         if (b + j < e) {
             const int c = static_cast<int>(cm.map(gcols[b + j]));
             if (c < 0) atomicExch(err, 1);
+            const int64_t d = c - (r + cm.halo_lo);
+            dist = max(dist, d < 0 ? -d : d);
             cols[slot] = c;
             vals[slot] = gvals[b + j];
         } else {
@@ -1329,6 +998,7 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ offs, const int64_t
             vals[slot] = M{};
         }
     }
+    if (dist > 0) atomicMax(band, static_cast<unsigned long long>(dist));
 }
 
 // ---- launch geometry -----------------------------------------------------------------------
@@ -1796,8 +1466,8 @@ void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d
     m.chunk_ptr.ensure(sizeof(int64_t) * (m.nchunks + 1));
     DeviceBuffer slots(sizeof(int64_t) * (m.nchunks + 1));
     m.chunk_full.ensure(static_cast<size_t>(m.nchunks) + 16);
-    DeviceBuffer dmax(sizeof(int) * 2);
-    CFD_CUDA(cudaMemsetAsync(dmax.p, 0, sizeof(int) * 2, st));
+    DeviceBuffer dmax(sizeof(int) * 4);  // max row length, error flag, band (uint64)
+    CFD_CUDA(cudaMemsetAsync(dmax.p, 0, sizeof(int) * 4, st));
     CFD_CUDA(cudaMemsetAsync(slots.p, 0, sizeof(int64_t) * (m.nchunks + 1), st));
     if (m.nchunks > 0) {
         sell_width_kernel<<<static_cast<unsigned>((m.nchunks + 255) / 256), 256, 0, st>>>(
@@ -1831,18 +1501,26 @@ void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d
             sell_fill_kernel<double2><<<grid, 256, 0, st>>>(
                 d_offs, d_cols, static_cast<const double2*>(d_vals), rows,
                 m.chunk_ptr.as<int64_t>(), m.cols.as<int>(), m.vals.as<double2>(), cm,
-                dmax.as<int>() + 1);
+                dmax.as<int>() + 1, reinterpret_cast<unsigned long long*>(dmax.as<int>() + 2));
         else
             sell_fill_kernel<double><<<grid, 256, 0, st>>>(
                 d_offs, d_cols, static_cast<const double*>(d_vals), rows,
                 m.chunk_ptr.as<int64_t>(), m.cols.as<int>(), m.vals.as<double>(), cm,
-                dmax.as<int>() + 1);
+                dmax.as<int>() + 1, reinterpret_cast<unsigned long long*>(dmax.as<int>() + 2));
         CFD_CUDA(cudaGetLastError());
     }
     int err = 0;
+    unsigned long long band = 0;
     CFD_CUDA(cudaMemcpyAsync(&err, dmax.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CFD_CUDA(cudaMemcpyAsync(&band, dmax.as<int>() + 2, sizeof(band), cudaMemcpyDeviceToHost, st));
     CFD_CUDA(cudaStreamSynchronize(st));
     if (err) fail(CHEBFD_ERR_UNSUPPORTED, "matrix column outside this rank's rows and halos");
+    m.band = static_cast<int64_t>(band);
+    // pair kernel tickets + one completion counter per 1024-row group, zeroed once
+    // (every launch leaves them zeroed)
+    const size_t groups = static_cast<size_t>((m.nchunks + 31) / 32);
+    m.pair_sync.ensure(sizeof(unsigned) * (2 + groups) + 16);
+    CFD_CUDA(cudaMemsetAsync(m.pair_sync.p, 0, m.pair_sync.bytes, st));
     // staged-gather plan (kernel variant 2): rows of width <= 16 only
     m.stage_max_rows = 0;
     if (m.nchunks > 0 && maxlen <= 16 && m.part.ext_rows() < (1LL << 31)) {

@@ -122,6 +122,42 @@ def test_apply_filter_bitexact_with_moments(ctx, orc, name, l, nb, deg, graphs):
         ctx.set_option("graphs", True)
 
 
+PAIR_CASES = [
+    ("ti", (4, 4, 4), 5, 9, {}), ("ti", (6, 5, 8), 32, 12, {"pair_tile_rows": 32}),
+    ("ti", (6, 6, 6), 16, 11, {"pair_slab": 5}), ("ti", (5, 6, 7), 8, 10, {"pair_extra": 0}),
+    ("graphene", (16, 16), 40, 10, {"pair_threads": 256}), ("graphene", (13, 7), 1, 7, {}),
+    ("graphene", (16, 16), 3, 8, {"pair_hints": 0}),
+]
+
+
+@pytest.mark.parametrize("name,l,nb,deg,knobs", PAIR_CASES)
+def test_apply_filter_pair_kernel_bitexact(ctx, orc, name, l, nb, deg, knobs):
+    """Two fused steps per launch (pair.cu, option pair=2): X bit-identical to the
+    oracle's apply_filter (filter.hpp:73-116), moments within 1e-12."""
+    ctx.set_option("pair", 2)
+    for k, v in knobs.items():
+        ctx.set_option(k, v)
+    try:
+        A, c = make_case(ctx, orc, name, l)
+        bounds = (-3.2, 3.3) if name == "graphene" else (-5.6, 5.6)
+        p = cf.make_filter((-0.2, 0.3), bounds, deg, "lanczos2")
+        x0 = orc.randomize(c.dim, nb, 19, name == "ti")
+        X = block(A, x0)
+        before = ctx.launch_count
+        mom = cf.apply_filter(A, X, p, want_moments=True)
+        launched = ctx.launch_count - before
+        xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+        assert bits_equal(X.to_numpy(), xr)
+        assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
+        # start-up steps + ceil((deg - 2) / 2) launches per column slab
+        if "pair_slab" not in knobs:
+            assert launched == 2 + (deg - 2 + 1) // 2
+    finally:
+        ctx.set_option("pair", 0)
+        for k in knobs:
+            ctx.set_option(k, -1 if k == "pair_extra" else (1 if k == "pair_hints" else 0))
+
+
 def test_apply_filter_host_e2e(ctx, orc):
     A, c = ti(ctx, orc, (4, 4, 3))
     p = cf.make_filter((-0.3, 0.3), (-5.6, 5.6), 30, "lanczos2")
@@ -130,6 +166,32 @@ def test_apply_filter_host_e2e(ctx, orc):
     cf.apply_filter_host(A, y, p)
     xr, _ = orc.apply_filter(c, x, p.combined, p.alpha, p.beta)
     assert bits_equal(y, xr)
+
+
+def test_filter_pipe_streams_bitexact(ctx, orc):
+    """chebfd_filter_pipe: five jobs in flight over two device slots (pinned and
+    pageable host blocks, in place and out of place) equal the oracle's filter."""
+    A, c = ti(ctx, orc, (5, 4, 6))
+    nb = 6
+    pipe = cf.FilterPipe(A, nb)
+    try:
+        ps = [cf.make_filter((-0.3, 0.2 + 0.05 * k), (-5.6, 5.6), 20 + 3 * k, "lanczos2")
+              for k in range(5)]
+        xs = [orc.randomize(c.dim, nb, 40 + k, True) for k in range(5)]
+        ins, outs = [], []
+        for k in range(5):
+            xin = cf.host_array(xs[k].shape, np.complex128) if k % 2 == 0 else xs[k].copy()
+            xin[:] = xs[k]
+            xout = xin if k < 3 else np.empty_like(xs[k])
+            pipe.submit(xin, ps[k], xout)
+            ins.append(xin)
+            outs.append(xout)
+        pipe.wait()
+        for k in range(5):
+            xr, _ = orc.apply_filter(c, xs[k], ps[k].combined, ps[k].alpha, ps[k].beta)
+            assert bits_equal(outs[k], xr), k
+    finally:
+        pipe.close()
 
 
 def test_block_equals_independent_columns(ctx, orc):
