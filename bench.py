@@ -146,7 +146,11 @@ def run_ours(args):
     target = (bounds.center() - 0.05 * hw, bounds.center() + 0.05 * hw)
     p = cf.make_filter(target, (bounds.lo, bounds.hi), Np, "lanczos2")
     X = cf.BlockVector(A, nb).randomize_device(7 + rank)
-    flops_apply, step_bytes = model_counts(D, nnz, nb, True, Np)
+    # whole-job flops from the global operator; the roofline's bytes are this rank's
+    # fused-step launch (its own rows and matrix entries)
+    Dl, nnz_l = A.local_rows, A.info["local_nnz"]
+    flops_apply, _ = model_counts(D, nnz, nb, True, Np)
+    _, step_bytes = model_counts(Dl, nnz_l, nb, True, Np)
     # ---- device-resident timed region -------------------------------------------
     for _ in range(args.warmup):
         cf.apply_filter(A, X, p)
@@ -170,7 +174,7 @@ def run_ours(args):
         ms_max = float(t[0])
         dist.barrier()
     ms_step = ms_max / args.steps
-    total_flops = flops_apply * world  # per step, all ranks (model counts are global / rank)
+    total_flops = flops_apply  # per step, all ranks (global operator)
     value = total_flops / (ms_step * 1e-3) / 1e9
     # fused-kernel roofline: algorithmic bytes per launch / average launch duration
     step_launch_ms = ms / (args.steps * Np)
@@ -179,11 +183,11 @@ def run_ours(args):
     # ---- end to end through the public C ABI with pinned host buffers ---------------
     lib = cf.load()
     host = C.c_void_p()
-    nbytes = D * nb * 16
+    nbytes = Dl * nb * 16  # this rank's rows
     assert lib.chebfd_host_alloc(nbytes, C.byref(host)) == 0
-    xh = np.ctypeslib.as_array((C.c_double * (2 * D * nb)).from_address(host.value))
-    xh[:] = np.random.default_rng(rank).standard_normal(2 * D * nb)
-    xc = xh.view(np.complex128).reshape(D, nb)
+    xh = np.ctypeslib.as_array((C.c_double * (2 * Dl * nb)).from_address(host.value))
+    xh[:] = np.random.default_rng(rank).standard_normal(2 * Dl * nb)
+    xc = xh.view(np.complex128).reshape(Dl, nb)
     for _ in range(max(1, args.warmup // 2)):
         cf.apply_filter_host(A, xc, p)
     if dist:
@@ -195,7 +199,7 @@ def run_ours(args):
     sync_s = (time.perf_counter() - t0) / e_steps
     # streamed: the same per-step host->device / device->host copies through
     # chebfd_filter_pipe, overlapped with the neighbouring steps' filters
-    xb = cf.host_array((D, nb), np.complex128)
+    xb = cf.host_array((Dl, nb), np.complex128)
     xb[:] = xc
     bufs = (xc, xb)
     pipe = cf.FilterPipe(A, nb)
@@ -346,8 +350,9 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded TI Hamiltonian, reference Gaussian block)",
         "config": {"workload": f"C2 TI 64^3 slab, n_b={args.nb}, N_p={args.degree} "
-                               "(BASELINE.json configs[1]); each timed step = a bounded sample "
-                               f"of {k} fused recurrence steps, rate-scaled"},
+                               "(BASELINE.json configs[1]; under torchrun the per-GPU 64^3 "
+                               "share of the weak-scaled lattice); each timed step = a bounded "
+                               f"sample of {k} fused recurrence steps, rate-scaled"},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
                          "kind": "reference",
                          "sample": f"{k} x {args.steps} spmmvm_fused steps on the reference "

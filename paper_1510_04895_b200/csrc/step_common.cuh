@@ -319,6 +319,43 @@ __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T w
     }
 }
 
+// ---- L2 eviction-priority hints (createpolicy + .L2::cache_hint) -------------------
+// mode 0: evict_normal, 1: evict_last, 2: evict_first
+__device__ __forceinline__ uint64_t l2_make_policy(int mode) {
+    uint64_t pol;
+    if (mode == 1)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else if (mode == 2)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// read-only (nc) load with an L2 policy
+__device__ __forceinline__ double ldg_pol(const double* p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ldg_pol(const double2* p, uint64_t pol) {
+    double2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+// coherent streaming load (no L1 allocation) with an L2 policy
+__device__ __forceinline__ double lds_pol(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 lds_pol(const double2* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 // ---- TMA bulk copies and mbarriers -------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
