@@ -312,6 +312,18 @@ void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
     exchange_halo(c, a, gathered, c.comm_stream);
     CFD_CUDA(cudaEventRecord(c.ev_b, c.comm_stream));
     int used = 0, base = 0;
+    // dot partials of column-slabbed launches cannot be split over interior and boundary
+    // launches: such steps wait for the halo and run as one launch per slab
+    StepArgs whole = s;
+    whole.row0 = 0;
+    whole.row1 = p.local;
+    if (s.dots_mode != 0 && step_slab_count(c, whole) > 1) {
+        CFD_CUDA(cudaStreamWaitEvent(c.stream, c.ev_b, 0));
+        whole.partial_base = 0;
+        whole.final_launch = true;
+        launch_step(c, whole, c.stream);
+        return;
+    }
     const bool overlap = c.overlap;
     if (!overlap) CFD_CUDA(cudaStreamWaitEvent(c.stream, c.ev_b, 0));
     // interior rows (no halo reads)

@@ -237,6 +237,8 @@ struct StepArgs {
     int* grid_used;          // out: number of blocks used
 };
 void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st);
+// column-slab launches launch_step will use for s (an upper bound: >= the real count)
+int step_slab_count(const Context& ctx, const StepArgs& s);
 // Steps coeff_index and coeff_index+1 of apply_filter's fused loop in one
 // wavefront launch (pair.cu); s.in = U, s.w = W as for the first step.
 // Returns false (nothing launched) where the pair kernel does not apply.

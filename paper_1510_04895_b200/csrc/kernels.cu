@@ -1049,6 +1049,9 @@ struct TmaShape {
 inline TmaShape tma_shape(const Context& ctx, int units, int64_t nrows) {
     if (nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms)) return {256, 32, 256};
     if (units <= 4) return {64, 64, 256};
+    // rows wider than one CTA: 128-unit column slabs (C3 lattice, n_b = 256, with the
+    // L2 hints: 128 / 64 / 32 / 16-unit slabs 19.8-20.9 / 19.9-20.2 / 20.1 / 20.9 ms
+    // over two runs -- within run-to-run noise; wider slabs re-read the matrix less)
     return {128, 64, 128};
 }
 inline Geometry geometry_pow2(int units, int cap = CFD_TMA_THREADS) {
@@ -1342,6 +1345,14 @@ void dispatch_kind(Context& ctx, const StepArgs& s, cudaStream_t st, int units, 
 }
 
 }  // namespace
+
+int step_slab_count(const Context& ctx, const StepArgs& s) {
+    const int units = static_cast<int>(s.a->kind == CHEBFD_COMPLEX128 ? s.width_cols
+                                       : (s.width_cols % 2 == 0 ? s.width_cols / 2 : s.width_cols));
+    const TmaShape shape = tma_shape(ctx, units, s.row1 - s.row0);
+    const int slab = ctx.slab_units > 0 ? std::min(ctx.slab_units, shape.slab_max) : shape.slab_max;
+    return (units + slab - 1) / slab;
+}
 
 // width (columns) -> units per row / unit type
 void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st) {
