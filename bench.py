@@ -270,7 +270,7 @@ def run_ours(args):
     return out
 
 
-NCU_SUMMARY_NAME = "profiles/r01_c2_fused_step.json"
+NCU_SUMMARY_NAME = "profiles/r01b_c2_fused_step.json"
 
 
 def ncu_traffic(w, nb, Np):
