@@ -96,7 +96,13 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count);
 enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_SLAB_UNITS = 5, CHEBFD_OPT_PAIR = 6, CHEBFD_OPT_PAIR_TILE_ROWS = 7,
        CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
-       CHEBFD_OPT_PAIR_SLAB = 11 };
+       CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12 };
+/* CHEBFD_OPT_MOMENTS: how apply_filter and kpm_dos form <x0, T_n(h) x0>: 0 one
+ * dot product against the kept x0 per step (the reference's way, filter.hpp:86-113,
+ * spectral.cpp:186-195); 1 (default) where the operator is bitwise Hermitian, the
+ * Chebyshev doubling identities T_2n = 2 T_n^2 - 1, T_2n+1 = 2 T_n T_n+1 - T_1: dots of
+ * the recurrence vectors already in registers, no x0 stream, and only the first half of
+ * the steps reduce (KPM: half the recurrence steps).  Equal up to rounding. */
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */

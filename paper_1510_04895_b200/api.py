@@ -157,10 +157,13 @@ class Context:
         """graphs (bool), overlap (bool), kernel ("gather" | "tma"),
         slab_units (int, 0 = 256), pair (0 off | 1 auto | 2 force: two fused
         steps per wavefront launch), pair_tile_rows / pair_threads /
-        pair_extra (pair-kernel tuning, 0 / 0 / -1 = automatic)."""
+        pair_extra (pair-kernel tuning, 0 / 0 / -1 = automatic), moments
+        ("direct" | "doubling": how filter / KPM moments are formed)."""
         code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5, "pair": 6,
                 "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
-                "pair_slab": 11}[name]
+                "pair_slab": 11, "moments": 12}[name]
+        if name == "moments" and isinstance(value, str):
+            value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):
             value = {"gather": 0, "tma": 1, "stage": 2, "tma2": 3}[value]
         _check(_lib().chebfd_ctx_set_option(self._h, code, int(value)))

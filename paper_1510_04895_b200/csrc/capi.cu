@@ -434,6 +434,7 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
     HostCsr csr = ti ? gen_topological_insulator(s, r0, r1) : gen_graphene(s, r0, r1);
     const int64_t nnz_g = allreduce_count(c, static_cast<int64_t>(csr.cols.size()));
     auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g);
+    m->hermitian = true;  // both models add every hopping with its conjugate (models.cpp:80-178)
     return m;
 }
 
@@ -476,21 +477,27 @@ FilterWorkspace& filter_workspace(Context& c, const Matrix& a, int64_t width, bo
 
 // Enqueue apply_filter (filter.hpp:73-116) on c.stream.  coeff_dev holds
 // combined[0..degree]; mom_dev (if moments) (degree+1) x width doubles.
+bool moment_doubling(const Context& c, const Matrix& a) { return c.moments_mode == 1 && a.hermitian; }
+
 void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double alpha, double beta,
                     const double* coeff_dev, double* mom_dev, FilterWorkspace& ws) {
     const bool moments = mom_dev != nullptr;
+    // doubling (DMODE 4): step n's registers give the raw sums of moments 2n-2, 2n-1, so
+    // only steps n <= degree/2 + 1 reduce and no x0 copy is kept (mom_dev has 2 spare rows)
+    const bool dbl = moments && moment_doubling(c, a);
     const int64_t nb = x.width;
-    // u = (alpha A + beta) x   [+ x0 = x, m0 = <x,x>, m1 = <x,u>]
+    // u = (alpha A + beta) x   [+ x0 = x (direct mode), m0 = <x,x>, m1 = <x,u>]
     StepArgs s{};
     s.kind_step = kStepSpmmvm;
     s.w = ws.u->owned();
-    s.x0 = moments ? ws.x0->owned() : nullptr;
+    s.x0 = moments && !dbl ? ws.x0->owned() : nullptr;
     s.alpha = alpha;
     s.beta = beta;
-    s.dots_mode = moments ? 3 : 0;
+    s.dots_mode = moments ? (dbl ? 4 : 3) : 0;
     s.dots_out = mom_dev;
     run_step_all(c, a, s, x);
-    // w = 2(alpha A + beta)u - x;  x = g0c0 x + g1c1 u + g2c2 w   [+ m2 = <x0,w>]
+    // w = 2(alpha A + beta)u - x;  x = g0c0 x + g1c1 u + g2c2 w   [+ m2 = <x0,w>; doubling:
+    // raw <u,u>, <u,w> for m2, m3]
     StepArgs s2{};
     s2.kind_step = kStepStart2;
     s2.w = ws.w->owned();
@@ -498,16 +505,18 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     s2.alpha = 2.0 * alpha;
     s2.beta = 2.0 * beta;
     s2.coeff_dev = coeff_dev;
-    s2.dots_mode = moments ? 2 : 0;
+    s2.dots_mode = moments ? (dbl ? 4 : 2) : 0;
     s2.dots_out = moments ? mom_dev + 2 * nb : nullptr;
     run_step_all(c, a, s2, *ws.u);
     Block* pu = ws.u.get();
     Block* pw = ws.w.get();
     for (int n = 3; n <= degree; ++n) {
         std::swap(pu, pw);  // swap handles, never copies
-        if (n < degree && run_pair_step(c, a, *pu, *pw, x, alpha, beta, coeff_dev, n,
-                                        moments ? ws.x0->owned() : nullptr,
-                                        moments ? mom_dev + static_cast<int64_t>(n) * nb : nullptr)) {
+        const bool dots_n = moments && (!dbl || 2 * n - 2 <= degree);
+        if (n < degree && !(dbl && dots_n) &&
+            run_pair_step(c, a, *pu, *pw, x, alpha, beta, coeff_dev, n,
+                          dots_n ? ws.x0->owned() : nullptr,
+                          dots_n ? mom_dev + static_cast<int64_t>(n) * nb : nullptr)) {
             // steps n and n+1 done: W holds V_n, U holds V_{n+1} -- the roles after step n+1
             std::swap(pu, pw);
             ++n;
@@ -517,13 +526,13 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
         f.kind_step = kStepFused;
         f.w = pw->owned();
         f.x = x.owned();
-        f.x0 = moments ? ws.x0->owned() : nullptr;
+        f.x0 = dots_n && !dbl ? ws.x0->owned() : nullptr;
         f.alpha = 2.0 * alpha;  // kernel multiplies values by (2 alpha) as kernels.hpp:95
         f.beta = 2.0 * beta;
         f.coeff_dev = coeff_dev;
         f.coeff_index = n;
-        f.dots_mode = moments ? 2 : 0;
-        f.dots_out = moments ? mom_dev + static_cast<int64_t>(n) * nb : nullptr;
+        f.dots_mode = dots_n ? (dbl ? 4 : 2) : 0;
+        f.dots_out = dots_n ? mom_dev + static_cast<int64_t>(dbl ? 2 * n - 2 : n) * nb : nullptr;
         run_step_all(c, a, f, *pu);
     }
     if (moments) allreduce_sum(c, mom_dev, static_cast<size_t>((degree + 1) * nb), c.stream);
@@ -534,8 +543,9 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
     check_conforms(a, x, "apply_filter");
     if (degree < 2) fail(CHEBFD_ERR_INVALID_ARGUMENT, "apply_filter: degree must be >= 2");
     const bool moments = moments_host != nullptr;
+    const bool dbl = moments && moment_doubling(c, a);
     const int64_t nb = x.width;
-    FilterWorkspace& ws = filter_workspace(c, a, nb, moments);
+    FilterWorkspace& ws = filter_workspace(c, a, nb, moments && !dbl);
     Matrix& am = const_cast<Matrix&>(a);
     if (c.kernel_variant >= 1) {  // pre-scaled values for the start step (alpha) and 2 alpha steps
         ensure_scaled_values(c, am, alpha, c.stream);
@@ -550,12 +560,17 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
     std::memcpy(&key.beta_bits, &beta, 8);
     const size_t coeff_bytes = sizeof(double) * (degree + 1);
     const size_t mom_bytes = sizeof(double) * (degree + 1) * std::max<int64_t>(nb, 1);
+    // doubling writes raw sums of moment pairs: up to two rows past the table
+    const size_t mom_alloc = mom_bytes + (dbl ? 2 * sizeof(double) * std::max<int64_t>(nb, 1) : 0);
+    auto finish_moments = [&] {
+        if (dbl) moments_from_doubling(moments_host, degree + 1, nb);
+    };
     if (c.use_graphs) {
         auto it = c.graphs.find(key);
         if (it == c.graphs.end()) {
             GraphEntry e;
             e.coeff = std::make_shared<DeviceBuffer>(coeff_bytes);
-            if (moments) e.moments = std::make_shared<DeviceBuffer>(mom_bytes);
+            if (moments) e.moments = std::make_shared<DeviceBuffer>(mom_alloc);
             CFD_CUDA(cudaMemcpyAsync(e.coeff->p, combined, coeff_bytes, cudaMemcpyHostToDevice,
                                      c.stream));
             ctx_sync(c);
@@ -586,6 +601,7 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
             CFD_CUDA(cudaMemcpyAsync(moments_host, it->second.moments->p, mom_bytes,
                                      cudaMemcpyDeviceToHost, c.stream));
             ctx_sync(c);
+            finish_moments();
         }
         return;
     }
@@ -593,13 +609,14 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
     CFD_CUDA(cudaMemcpyAsync(c.coeffs.p, combined, coeff_bytes, cudaMemcpyHostToDevice, c.stream));
     double* mom_dev = nullptr;
     if (moments) {
-        c.dscratch.ensure(mom_bytes);
+        c.dscratch.ensure(mom_alloc);
         mom_dev = c.dscratch.as<double>();
     }
     enqueue_filter(c, a, x, degree, alpha, beta, c.coeffs.as<double>(), mom_dev, ws);
     if (moments) {
         CFD_CUDA(cudaMemcpyAsync(moments_host, mom_dev, mom_bytes, cudaMemcpyDeviceToHost, c.stream));
         ctx_sync(c);
+        finish_moments();
     }
 }
 
@@ -664,8 +681,8 @@ static void ctx_init(Context& c, int device) {
     // inside graph capture): grid <= 8 CTAs/SM, up to 3 launches per step,
     // 2 dots x 256 units x 16 B
     c.partials.ensure(static_cast<size_t>(c.num_sms) * 8 * 3 * 2 * 256 * 16);
-    c.counter.ensure(256);
-    CFD_CUDA(cudaMemsetAsync(c.counter.p, 0, 256, c.stream));
+    c.counter.ensure(4096);  // grid ticket + group tickets of grid_reduce
+    CFD_CUDA(cudaMemsetAsync(c.counter.p, 0, 4096, c.stream));
     c.dscratch.ensure(1 << 20);
     ctx_sync(c);
 }
@@ -742,6 +759,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->slab_units = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR)
             c->pair_mode = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_MOMENTS)
+            c->moments_mode = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
             c->pair_tile_rows = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_THREADS)
@@ -846,6 +865,7 @@ int chebfd_matrix_from_csr(chebfd_ctx* ctx, int kind, int64_t dim, const int64_t
         const double* v = static_cast<const double*>(vals);
         h.vals.assign(v + f * offs[r0], v + f * offs[r1]);
         auto m = matrix_from_host_csr(c, h, r0, r1, starts, nnz);
+        m->hermitian = csr_is_hermitian(kind, dim, offs, cols, v);
         *out = reinterpret_cast<chebfd_matrix*>(m.release());
     });
 }

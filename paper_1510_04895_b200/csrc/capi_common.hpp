@@ -38,6 +38,8 @@ void check_same_shape(const Block& x, const Block& y);
 // BlockVector::randomize of this rank's rows, streamed host -> device
 void randomize_upload(Context& c, Block& b, uint64_t seed);
 void check_conforms(const Matrix& a, const Block& x, const char* who);
+// moments by the Chebyshev doubling identities (CHEBFD_OPT_MOMENTS, Hermitian operators)
+bool moment_doubling(const Context& c, const Matrix& a);
 void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered);
 void allreduce_sum(Context& c, double* dev, size_t n, cudaStream_t st);
 void column_dots_host(Context& c, const Block& x, const Block& y, void* out);

@@ -209,6 +209,33 @@ HostCsr gen_topological_insulator(const chebfd_lattice& s, int64_t r0, int64_t r
 }
 
 // window_coeffs (filter.cpp:43-56)
+bool csr_is_hermitian(int kind, int64_t dim, const int64_t* offs, const int64_t* cols,
+                      const double* vals) {
+    for (int64_t i = 0; i < dim; ++i) {
+        for (int64_t p = offs[i]; p < offs[i + 1]; ++p) {
+            const int64_t j = cols[p];
+            int64_t hit = -1, count = 0;
+            for (int64_t q = offs[j]; q < offs[j + 1]; ++q)
+                if (cols[q] == i) {
+                    if (hit < 0) hit = q;
+                    ++count;
+                }
+            if (count != 1) return false;
+            if (kind) {
+                if (vals[2 * p] != vals[2 * hit] || vals[2 * p + 1] != -vals[2 * hit + 1]) return false;
+            } else if (vals[p] != vals[hit]) {
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
+void moments_from_doubling(double* m, int64_t rows, int64_t width) {
+    for (int64_t q = 2; q < rows; ++q)
+        for (int64_t k = 0; k < width; ++k) m[q * width + k] = 2.0 * m[q * width + k] - m[(q & 1) * width + k];
+}
+
 std::vector<double> window_coeffs(double tlo, double thi, double blo, double bhi, int degree) {
     if (!(tlo < thi)) fail(CHEBFD_ERR_INVALID_ARGUMENT, "degenerate target interval");
     if (!(blo < bhi)) fail(CHEBFD_ERR_INVALID_ARGUMENT, "degenerate bounds interval");

@@ -115,6 +115,8 @@ struct Matrix {
     // and 2 alpha); at most 4 are kept
     std::vector<std::pair<double, std::unique_ptr<DeviceBuffer>>> scaled;
     bool scaled_evicted = false;
+    bool hermitian = false; // bitwise A = A^H (lattice models; checked for from_csr input):
+                            // enables moment doubling
     int64_t band = 0;       // max |extended column - extended row| over all entries
     DeviceBuffer pair_sync; // pair kernel: item / exit tickets + per-1024-row group counters (zeroed)
 };
@@ -182,6 +184,9 @@ struct Context {
     int slab_units = 0;   // step kernel column-slab width in 16-byte units (0: up to 256)
     // two fused steps per launch (pair.cu): 0 off, 1 where the wavefront's working set
     // fits the L2, 2 wherever the kernel applies; tuning knobs (0 / -1: automatic)
+    // filter / KPM moments: 0 direct <x0, T_n x0> per step (x0 stream), 1 doubling from
+    // <V_n, V_n>, <V_n, V_n+1> where the operator is Hermitian (default)
+    int moments_mode = 1;
     int pair_mode = 0, pair_tile_rows = 0, pair_threads = 0, pair_extra = -1, pair_hints = 1,
         pair_slab = 0;
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
@@ -274,6 +279,11 @@ struct HostCsr {
     std::vector<double> vals;         // interleaved for complex
 };
 HostCsr gen_graphene(const chebfd_lattice& s, int64_t r0, int64_t r1);
+// bitwise Hermitian test of a whole CSR (every (i,j,v) has (j,i,conj v); no duplicate columns)
+bool csr_is_hermitian(int kind, int64_t dim, const int64_t* offs, const int64_t* cols,
+                      const double* vals);
+// moment doubling (DMODE 4) raw sums -> moments: rows q >= 2 become 2 raw - m(q mod 2)
+void moments_from_doubling(double* m, int64_t rows, int64_t width);
 HostCsr gen_topological_insulator(const chebfd_lattice& s, int64_t r0, int64_t r1);
 void validate_lattice(const chebfd_lattice& s, bool needs_z);
 // std::mt19937_64 + std::normal_distribution stream (block_vector.hpp:42-51):

@@ -47,7 +47,7 @@ template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 __global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
     const int t = threadIdx.x;
     const int rr = t / p.US;
     const int u = t - rr * p.US;
@@ -130,7 +130,7 @@ template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
     const int t = threadIdx.x;
@@ -143,6 +143,14 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
     const int cap = MAXW * TR;  // slots per buffer
     int* cols_s = reinterpret_cast<int*>(smem_raw);
     M* vals_s = reinterpret_cast<M*>(smem_raw + ((2 * cap * sizeof(int) + 15) & ~size_t(15)));
+    // plain dot sums (modes 2-4) accumulate in shared memory, one slot per thread and
+    // dot, so no accumulator register is live across a row's gathers (C2, two moment
+    // dots per row: 734 us per step with complex register accumulators -- ptxas split
+    // the eleven gathers into two batches --, 713 us with real-part registers, 685 us
+    // here; no dots: 587 us)
+    constexpr bool SACC = NDOT > 0 && DMODE != 1;
+    auto* sacc = reinterpret_cast<std::conditional_t<DMODE == 1, T, typename O::DT>*>(
+        smem_raw + ((((2 * cap * sizeof(int) + 15) & ~size_t(15)) + 2 * cap * sizeof(M) + 15) & ~size_t(15)));
 
     const int cu = p.u_off + u;
     const T* __restrict__ inu = static_cast<const T*>(p.in) + cu;
@@ -159,12 +167,15 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
         c1 = p.coeff_dev[1];
         c2 = p.coeff_dev[2];
     }
-    T acc_d[NDOT > 0 ? NDOT : 1];
-    T comp_d[NDOT > 0 ? NDOT : 1];
+    // dot accumulators: Kahan <x, w> (mode 1) keeps complex units; moments and plain
+    // dots only need real parts (O::DT)
+    using A = std::conditional_t<DMODE == 1, T, typename O::DT>;
+    A acc_d[NDOT > 0 ? NDOT : 1];
+    A comp_d[NDOT > 0 ? NDOT : 1];
 #pragma unroll
     for (int d = 0; d < (NDOT > 0 ? NDOT : 1); ++d) {
-        acc_d[d] = O::zero();
-        comp_d[d] = O::zero();
+        acc_d[d] = A{};
+        comp_d[d] = A{};
     }
 
 #if CFD_L2_HINTS
@@ -238,10 +249,25 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
                 if (c[j] >= 0) acc = O::vadd(acc, O::prod(vs[coff + j * 32], g[j]));
         }
         const T ui = ldg(&inu[(r + halo) * pitch]);
-        step_epilogue<O, T, KIND, DMODE>(acc, ui, wi, xi, x0v, own, W, X, X0, p.beta, coeff, c1,
-                                         c2, acc_d, comp_d);
+        if constexpr (SACC) {
+            A dl[NDOT], dc[NDOT];
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d) dl[d] = dc[d] = A{};
+            step_epilogue<O, T, KIND, DMODE>(acc, ui, wi, xi, x0v, own, W, X, X0, p.beta, coeff, c1,
+                                             c2, dl, dc);
+            // 0 + v is exact: the same roundings as accumulating in a register
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d) sacc[d * blockDim.x + t] = tadd(sacc[d * blockDim.x + t], dl[d]);
+        } else {
+            step_epilogue<O, T, KIND, DMODE>(acc, ui, wi, xi, x0v, own, W, X, X0, p.beta, coeff, c1,
+                                             c2, acc_d, comp_d);
+        }
     };
 
+    if constexpr (SACC) {
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) sacc[d * blockDim.x + t] = A{};
+    }
     if (t == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -279,16 +305,17 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
     }
 
     if constexpr (NDOT > 0) {
-        T acc_out[NDOT];
+        A acc_out[NDOT];
 #pragma unroll
-        for (int d = 0; d < NDOT; ++d) acc_out[d] = acc_d[d];
+        for (int d = 0; d < NDOT; ++d) acc_out[d] = SACC ? sacc[d * blockDim.x + t] : acc_d[d];
+        __syncthreads();  // grid_reduce reuses the shared memory
         const int uoff = p.u_off;
         void* outp = p.dots_out;
         const int64_t dstride = p.dots_row_stride;
-        grid_reduce<T, NDOT>(acc_out, R, US, static_cast<T*>(p.partials), p.part_base + blockIdx.x,
+        grid_reduce<A, NDOT>(acc_out, R, US, static_cast<A*>(p.partials), p.part_base + blockIdx.x,
                              p.nparts, p.final_launch != 0, p.counter,
-                             [&](int d, int uu, T vv) {
-                                 if (DMODE == 1)
+                             [&](int d, int uu, A vv) {
+                                 if constexpr (DMODE == 1)
                                      O::store_full(static_cast<T*>(outp), uoff + uu, vv);
                                  else
                                      O::store_re(static_cast<double*>(outp) + d * dstride,
@@ -337,7 +364,7 @@ __device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, c
         T y = acc;
         if (beta != 0.0) y = O::vadd(y, O::smul(beta, ui));  // kernels.hpp:62-65
         w_out = y;
-        if constexpr (DMODE == 3) {
+        if constexpr (DMODE == 3 || DMODE == 4) {
             x0_out = ui;
             acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, ui));
             acc_d[1] = O::vadd(acc_d[1], O::cdot(ui, y));
@@ -348,6 +375,7 @@ __device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, c
         const T wn = O::vadd(O::vadd(O::smul(1.0, wr), O::smul(-1.0, xi)), O::smul(0.0, xi));
         w_out = wn;
         if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(xi, wn));
+        if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
         x_out = O::vadd(O::vadd(O::smul(coeff, xi), O::smul(c1, ui)), O::smul(c2, wn));
     } else {
         const T wn = O::vsub(O::vadd(acc, O::smul(beta, ui)), wi);
@@ -359,6 +387,7 @@ __device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, c
         } else {
             if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
         }
+        if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
     }
 }
 
@@ -368,7 +397,7 @@ __global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
     using P = U2<T>;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
     constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
     constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
     constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
@@ -574,7 +603,7 @@ __global__ void __launch_bounds__(256, 1) step_stage_kernel(const StepParams p, 
     using O = Ops<CPLX, T>;
     using M = typename O::M;
     constexpr int US = 32, R = 8, NP = 4;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
     constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
     constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
     constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
@@ -1074,7 +1103,7 @@ int max_blocks_for(K kernel, int threads, size_t smem, int num_sms) {
 template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
     const Matrix& a = *s.a;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE == 3 ? 2 : 1);
+    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
     const int64_t nrows = s.row1 - s.row0;
     constexpr int MW = MAXW > 0 ? MAXW : 4;
     const void* svals = s.alpha == 1.0 ? a.vals.p : find_scaled(a, s.alpha);
@@ -1082,7 +1111,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     auto kernel = tma ? step_tma_kernel<CPLX, T, KIND, DMODE, MW>
                       : step_kernel<CPLX, T, KIND, DMODE, 0>;
     int used_total = 0;
-    if constexpr (MAXW >= 8 && std::is_same_v<T, double2>) {
+    if constexpr (MAXW >= 8 && std::is_same_v<T, double2> && DMODE != 4) {
         // staged-gather kernel: one 512-byte row slot, plan present and fitting shared memory
         if (ctx.kernel_variant == 2 && tma && units == 32 && pitch == 32 && a.stage_max_rows > 0 &&
             nrows > 0) {
@@ -1130,9 +1159,9 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
                 p.dots_row_stride = static_cast<int64_t>(units) * Ops<CPLX, T>::kCols;
                 if (NDOT > 0) {
                     const size_t need_bytes =
-                        static_cast<size_t>(s.partial_base + grid) * NDOT * 32 * sizeof(T);
+                        static_cast<size_t>(reduce_rows_needed(s.partial_base + grid)) * NDOT * 32 * sizeof(T);
                     ctx.partials.ensure(std::max<size_t>(need_bytes, 1 << 20));
-                    ctx.counter.ensure(256);
+                    ctx.counter.ensure(4096);
                 }
                 p.partials = ctx.partials.p;
                 p.part_base = s.partial_base;
@@ -1212,9 +1241,9 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
             p.dots_row_stride = static_cast<int64_t>(units) * Ops<CPLX, T>::kCols;
             if (NDOT > 0) {
                 const size_t need_bytes =
-                    static_cast<size_t>(s.partial_base + grid) * NDOT * units * sizeof(T);
+                    static_cast<size_t>(reduce_rows_needed(s.partial_base + grid)) * NDOT * units * sizeof(T);
                 ctx.partials.ensure(std::max<size_t>(need_bytes, 1 << 20));
-                ctx.counter.ensure(256);
+                ctx.counter.ensure(4096);
             }
             p.partials = ctx.partials.p;
             p.part_base = s.partial_base;
@@ -1239,6 +1268,9 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         const size_t stage = tma ? 2 * static_cast<size_t>(MW) * TR : 0;
         size_t ring = tma ? ((stage * sizeof(int) + 15) & ~size_t(15)) + stage * (CPLX ? 16 : 8)
                           : 0;
+        // the TMA kernel's shared dot accumulators follow the ring (modes 2-4)
+        if (tma && NDOT > 0 && DMODE != 1)
+            ring = ((ring + 15) & ~size_t(15)) + NDOT * static_cast<size_t>(g.threads) * sizeof(T);
         const size_t smem = std::max(NDOT * static_cast<size_t>(g.threads) * sizeof(T), ring);
         if (smem > 48 * 1024) {
             static thread_local std::map<const void*, size_t> attr_set;
@@ -1290,10 +1322,10 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         p.dots_row_stride = static_cast<int64_t>(units) * Ops<CPLX, T>::kCols;  // = nb columns
         if (NDOT > 0) {
             const size_t need_bytes =
-                static_cast<size_t>(s.partial_base + grid) * NDOT * us * sizeof(T);
+                static_cast<size_t>(reduce_rows_needed(s.partial_base + grid)) * NDOT * us * sizeof(T);
             // partials are slab-local: slabs run sequentially on the stream
             ctx.partials.ensure(std::max<size_t>(need_bytes, 1 << 20));
-            ctx.counter.ensure(256);
+            ctx.counter.ensure(4096);
         }
         p.partials = ctx.partials.p;
         p.part_base = s.partial_base;
@@ -1318,16 +1350,20 @@ void dispatch_kind_w(Context& ctx, const StepArgs& s, cudaStream_t st, int units
     switch (s.kind_step) {
         case kStepSpmmvm:
             if (s.dots_mode == 3) return run_step<CPLX, T, kStepSpmmvm, 3, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 4) return run_step<CPLX, T, kStepSpmmvm, 4, MAXW>(ctx, s, st, units, pitch);
             return run_step<CPLX, T, kStepSpmmvm, 0, MAXW>(ctx, s, st, units, pitch);
         case kStepStart2:
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepStart2, 2, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 4) return run_step<CPLX, T, kStepStart2, 4, MAXW>(ctx, s, st, units, pitch);
             return run_step<CPLX, T, kStepStart2, 0, MAXW>(ctx, s, st, units, pitch);
         case kStepFused:
             if (s.dots_mode == 1) return run_step<CPLX, T, kStepFused, 1, MAXW>(ctx, s, st, units, pitch);
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepFused, 2, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 4) return run_step<CPLX, T, kStepFused, 4, MAXW>(ctx, s, st, units, pitch);
             return run_step<CPLX, T, kStepFused, 0, MAXW>(ctx, s, st, units, pitch);
         case kStepRecur:
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepRecur, 2, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 4) return run_step<CPLX, T, kStepRecur, 4, MAXW>(ctx, s, st, units, pitch);
             return run_step<CPLX, T, kStepRecur, 0, MAXW>(ctx, s, st, units, pitch);
     }
     fail(CHEBFD_ERR_INVALID_ARGUMENT, "bad step kind");
@@ -1407,8 +1443,9 @@ void run_colreduce(Context& ctx, const Block& x, const Block& y, const double* l
         const int maxb = max_blocks_for(kernel, g.threads, smem, ctx.num_sms);
         const int64_t need = (x.rows + g.R - 1) / g.R;
         const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, maxb)));
-        ctx.partials.ensure(std::max<size_t>(static_cast<size_t>(grid) * us * sizeof(T), 1 << 20));
-        ctx.counter.ensure(256);
+        ctx.partials.ensure(
+            std::max<size_t>(static_cast<size_t>(reduce_rows_needed(grid)) * us * sizeof(T), 1 << 20));
+        ctx.counter.ensure(4096);
         kernel<<<grid, g.threads, smem, st>>>(
             static_cast<const T*>(x.owned()), static_cast<const T*>(y.owned()), lam, x.rows,
             units, u0, us, g.R, out, ctx.partials.as<T>(), ctx.counter.as<unsigned>());

@@ -440,8 +440,9 @@ bool run_pair(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     }
     if (NDOT > 0) {
         ctx.partials.ensure(
-            std::max<size_t>(static_cast<size_t>(g.grid) * NDOT * units * sizeof(T), 1 << 20));
-        ctx.counter.ensure(256);
+            std::max<size_t>(static_cast<size_t>(reduce_rows_needed(g.grid)) * NDOT * units * sizeof(T),
+                             1 << 20));
+        ctx.counter.ensure(4096);
     }
     for (int u0 = 0; u0 < units; u0 += w) {
         PairParams q{};

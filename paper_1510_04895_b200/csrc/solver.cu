@@ -237,7 +237,11 @@ std::vector<double> kpm_dos(Context& c, const Matrix& a, double blo, double bhi,
     auto u = make_block(c, &a, a.kind, a.part.local, samples, false);
     auto w = make_block(c, &a, a.kind, a.part.local, samples, false);
     const int nchecks = order / 128;
-    DeviceBuffer mom(sizeof(double) * (order + 1) * samples);
+    // doubling: recurrence step n (V_n from V_n-1) yields the raw sums of moments 2n-2 and
+    // 2n-1 (<V_n-1, V_n-1>, <V_n-1, V_n>), so order/2 + 1 steps give all order + 1 moments
+    const bool dbl = moment_doubling(c, a);
+    const int last_step = dbl ? order / 2 + 1 : order;
+    DeviceBuffer mom(sizeof(double) * (order + 3) * samples);
     const size_t nrm_row = static_cast<size_t>(samples) * (a.kind ? 2 : 1);
     DeviceBuffer nrm(sizeof(double) * std::max<size_t>(nrm_row * nchecks, 1));
     // u = h z; w = z (x0 copy); dots rows 0 (<z,z>), 1 (<z,u>)
@@ -252,16 +256,16 @@ std::vector<double> kpm_dos(Context& c, const Matrix& a, double blo, double bhi,
     run_step_all(c, a, s, *z);
     Block* pu = u.get();
     Block* pw = w.get();
-    for (int n = 2; n <= order; ++n) {
+    for (int n = 2; n <= last_step; ++n) {
         if (n > 2) std::swap(pu, pw);
         StepArgs r{};
         r.kind_step = kStepRecur;
         r.w = pw->owned();
-        r.x0 = z->owned();
+        r.x0 = dbl ? nullptr : z->owned();
         r.alpha = 2.0 * alpha;
         r.beta = 2.0 * beta;
-        r.dots_mode = 2;
-        r.dots_out = mom.as<double>() + static_cast<int64_t>(n) * samples;
+        r.dots_mode = dbl ? 4 : 2;
+        r.dots_out = mom.as<double>() + static_cast<int64_t>(dbl ? 2 * n - 2 : n) * samples;
         run_step_all(c, a, r, *pu);
         if (n % 128 == 0)
             launch_column_reduce(c, *pw, *pw, 0, nrm.as<double>() + (n / 128 - 1) * nrm_row, c.stream);
@@ -275,6 +279,7 @@ std::vector<double> kpm_dos(Context& c, const Matrix& a, double blo, double bhi,
         CFD_CUDA(cudaMemcpyAsync(hn.data(), nrm.p, hn.size() * sizeof(double), cudaMemcpyDeviceToHost,
                                  c.stream));
     ctx_sync(c);
+    if (dbl) moments_from_doubling(hm.data(), order + 1, samples);
     const double scale = static_cast<double>(d) / samples;
     std::vector<double> mu(static_cast<size_t>(order) + 1, 0.0);
     mu[0] = static_cast<double>(d);
@@ -284,7 +289,7 @@ std::vector<double> kpm_dos(Context& c, const Matrix& a, double blo, double bhi,
         mu[n] = scale * sum;
         if (!std::isfinite(mu[n]) || std::abs(mu[n]) > 4.0 * d)
             fail(CHEBFD_ERR_RUNTIME, "kpm_dos: moment growth indicates spectrum outside bounds");
-        if (n % 128 == 0) {
+        if (n % 128 == 0 && n <= last_step) {
             for (int k = 0; k < samples; ++k) {
                 const double v = std::sqrt(hn[(n / 128 - 1) * nrm_row + (a.kind ? 2 * k : k)]);
                 if (!std::isfinite(v) || v > 4.0)

@@ -42,6 +42,8 @@ struct Ops<false, double> {
     __device__ static double vsub(double a, double b) { return sub(a, b); }
     __device__ static double smul(double s, double v) { return mul(s, v); }
     __device__ static double cdot(double x, double w) { return mul(x, w); }
+    using DT = double;  // moment / plain-dot accumulator
+    __device__ static double cdot_re(double x, double w) { return mul(x, w); }
     __device__ static double lam_mul(const double* lam, int col, double v) { return mul(lam[col], v); }
     __device__ static double cdiv(double v, const double* d, int col) { return div_(v, d[col]); }
     __device__ static void store_re(double* out, int unit, double v) { out[unit] = v; }
@@ -60,6 +62,8 @@ struct Ops<false, double2> {
     __device__ static double2 vsub(double2 a, double2 b) { return make_double2(sub(a.x, b.x), sub(a.y, b.y)); }
     __device__ static double2 smul(double s, double2 v) { return make_double2(mul(s, v.x), mul(s, v.y)); }
     __device__ static double2 cdot(double2 x, double2 w) { return make_double2(mul(x.x, w.x), mul(x.y, w.y)); }
+    using DT = double2;  // two real columns: both products are moments
+    __device__ static double2 cdot_re(double2 x, double2 w) { return cdot(x, w); }
     __device__ static double2 lam_mul(const double* lam, int col, double2 v) {
         return make_double2(mul(lam[col], v.x), mul(lam[col + 1], v.y));
     }
@@ -93,6 +97,13 @@ struct Ops<true, double2> {
         const double nxi = -x.y;
         return make_double2(sub(mul(x.x, w.x), mul(nxi, w.y)), add(mul(x.x, w.y), mul(nxi, w.x)));
     }
+    // Re(conj(x) w) alone (moments are real parts): the same bits as cdot(x, w).x
+    using DT = double;
+    __device__ static double cdot_re(double2 x, double2 w) {
+        const double nxi = -x.y;
+        return sub(mul(x.x, w.x), mul(nxi, w.y));
+    }
+    __device__ static void store_re(double* out, int unit, double v) { out[unit] = v; }
     __device__ static double2 lam_mul(const double* lam, int col, double2 v) { return smul(lam[col], v); }
     __device__ static double2 cdiv(double2 v, const double* d, int col) {
         return make_double2(div_(v.x, d[col]), div_(v.y, d[col]));
@@ -137,9 +148,18 @@ __device__ __forceinline__ T ldcg_t(const T* p) {
 }
 
 // ---- fixed-order block + grid reduction of NDOT per-unit accumulators -------------
-// Threads are laid out t = rr*US + u.  Each CTA writes NDOT*US partials; the
-// last CTA to finish (ticket) sums partial rows [0, nparts) in order and
-// hands the totals to `emit(d, u, value)`.
+// Threads are laid out t = rr*US + u.  Each CTA writes NDOT*US partials.  When all
+// partials come from this launch, the last CTA of every group of kReduceGroup CTAs sums
+// its group's partials in index order, and the last group to finish sums the group
+// sums in order (two short reductions instead of one CTA reading every partial while
+// the GPU idles).  A launch that completes partials of earlier launches
+// (interior + boundary rows) sums rows [0, nparts) in order in its last CTA.  Either
+// way the order -- hence every bit -- is fixed, and `emit(d, u, value)` gets the totals.
+// counter[0]: grid ticket, counter[1 + g]: group tickets; all self-resetting.
+constexpr int kReduceGroup = 32;
+// partial rows a grid reduction over n CTA partials needs (its group sums included)
+__host__ __device__ constexpr int64_t reduce_rows_needed(int64_t n) { return n + (n + kReduceGroup - 1) / kReduceGroup; }
+
 template <class T, int NDOT, class Emit>
 __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1], int R, int US,
                                             T* partials, int part_slot, int nparts, bool final_launch,
@@ -164,42 +184,78 @@ __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1],
     __threadfence();
     __syncthreads();
     __shared__ unsigned is_last;
-    if (t == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-#pragma unroll
-    for (int d = 0; d < NDOT; ++d) {
-        // partials rr, rr + R, rr + 2R, ... summed left to right; eight loads in
-        // flight per step (the order, hence every bit, is the sequential loop's)
-        auto at = [&](int q) {
-            return ldcg_t(&partials[(static_cast<int64_t>(q) * NDOT + d) * US + u]);
-        };
-        T s = T{};
-        int q = rr;
-        if (q < nparts) {
-            s = at(q);
-            q += R;
-        }
-        for (; q + 7 * R < nparts; q += 8 * R) {
-            T v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = at(q + k * R);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) s = tadd(s, v[k]);
-        }
-        for (; q < nparts; q += R) s = tadd(s, at(q));
-        sred[d * nthr + t] = s;
-    }
-    __syncthreads();
-    if (rr == 0) {
+    // rows [first, first + count) of src (NDOT x US each) summed in index order; the
+    // totals land in sred[d * nthr + u] (rr == 0 threads hold them after the call)
+    auto reduce_rows = [&](const T* src, int first, int count) {
 #pragma unroll
         for (int d = 0; d < NDOT; ++d) {
-            T s = sred[d * nthr + u];
-            const int lim = R < nparts ? R : nparts;
-            for (int q = 1; q < lim; ++q) s = tadd(s, sred[d * nthr + q * US + u]);
-            emit(d, u, s);
+            // rows rr, rr + R, rr + 2R, ... left to right, eight loads in flight
+            auto at = [&](int q) {
+                return ldcg_t(&src[(static_cast<int64_t>(first + q) * NDOT + d) * US + u]);
+            };
+            T s = T{};
+            int q = rr;
+            if (q < count) {
+                s = at(q);
+                q += R;
+            }
+            for (; q + 7 * R < count; q += 8 * R) {
+                T v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = at(q + k * R);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) s = tadd(s, v[k]);
+            }
+            for (; q < count; q += R) s = tadd(s, at(q));
+            sred[d * nthr + t] = s;
         }
+        __syncthreads();
+        if (rr == 0) {
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d) {
+                T s = sred[d * nthr + u];
+                const int lim = R < count ? R : count;
+                for (int q = 1; q < lim; ++q) s = tadd(s, sred[d * nthr + q * US + u]);
+                sred[d * nthr + u] = s;
+            }
+        }
+    };
+    const bool two_level = nparts == static_cast<int>(gridDim.x) && part_slot == static_cast<int>(blockIdx.x);
+    if (two_level) {
+        const int g = static_cast<int>(blockIdx.x) / kReduceGroup;
+        const int gsize = min(kReduceGroup, nparts - g * kReduceGroup);
+        const int ngroups = (nparts + kReduceGroup - 1) / kReduceGroup;
+        if (t == 0) is_last = (atomicAdd(&counter[1 + g], 1u) == static_cast<unsigned>(gsize - 1));
+        __syncthreads();
+        if (!is_last) return;
+        __threadfence();
+        T* gpart = partials + static_cast<int64_t>(nparts) * NDOT * US;
+        reduce_rows(partials, g * kReduceGroup, gsize);
+        if (rr == 0) {
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d)
+                gpart[(static_cast<int64_t>(g) * NDOT + d) * US + u] = sred[d * nthr + u];
+        }
+        __threadfence();
+        __syncthreads();
+        if (t == 0) {
+            counter[1 + g] = 0u;
+            is_last = (atomicAdd(counter, 1u) == static_cast<unsigned>(ngroups - 1));
+        }
+        __syncthreads();
+        if (!is_last) return;
+        __threadfence();
+        reduce_rows(gpart, 0, ngroups);
+    } else {
+        if (t == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+        __syncthreads();
+        if (!is_last) return;
+        __threadfence();
+        reduce_rows(partials, 0, nparts);
+    }
+    if (rr == 0) {
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) emit(d, u, sred[d * nthr + u]);
     }
     if (t == 0) *counter = 0u;  // self-reset for the next stream-ordered launch
 }
@@ -281,20 +337,41 @@ __device__ __forceinline__ T gather_row(const int* __restrict__ cols, const M* _
 }
 
 // Per-entry epilogue of each step kind, in the reference's operation order.
-template <class O, class T, int KIND, int DMODE, int NA>
+// Moment doubling (DMODE 4): for Hermitian h, V_n = T_n(h) x0 gives
+//   <x0, T_{2n} x0> = 2 <V_n, V_n> - <x0, x0>,  <x0, T_{2n+1} x0> = 2 <V_n, V_{n+1}> - <x0, T_1 x0>
+// so the step producing V_{n+1} from V_n (own row ui, result wn) yields the raw sums for
+// moments 2n and 2n+1 from registers: no x0 stream, and only the first half of a filter's
+// steps reduce at all.  The host applies 2 raw - m0 / 2 raw - m1 (capi.cu).
+// acc += <x, w> in the accumulator's type: the full product for unit-typed (T)
+// accumulators, its real part alone for O::DT ones (same bits as the product's .x)
+template <class O, class A, class T>
+__device__ __forceinline__ void dot_acc(A& acc, const T x, const T w) {
+    if constexpr (std::is_same_v<A, T>)
+        acc = O::vadd(acc, O::cdot(x, w));
+    else
+        acc = add(acc, O::cdot_re(x, w));
+}
+
+template <class O, class A, class T, int NA>
+__device__ __forceinline__ void moment_pair(A (&acc_d)[NA], const T ui, const T wn) {
+    dot_acc<O>(acc_d[0], ui, ui);
+    dot_acc<O>(acc_d[1], ui, wn);
+}
+
+template <class O, class T, int KIND, int DMODE, class A, int NA>
 __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T wi, const T xi,
                                               const T x0v, int64_t own, T* __restrict__ W,
                                               T* __restrict__ X, T* __restrict__ X0, double beta,
-                                              double coeff, double c1, double c2, T (&acc_d)[NA],
-                                              T (&comp_d)[NA]) {
+                                              double coeff, double c1, double c2, A (&acc_d)[NA],
+                                              A (&comp_d)[NA]) {
     if constexpr (KIND == kStepSpmmvm) {
         T y = acc;
         if (beta != 0.0) y = O::vadd(y, O::smul(beta, ui));  // kernels.hpp:62-65
         st_stream(&W[own], y);
-        if constexpr (DMODE == 3) {  // apply_filter entry: x0 = X, m0 = <x,x>, m1 = <x,u>
-            st_stream(&X0[own], ui);
-            acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, ui));
-            acc_d[1] = O::vadd(acc_d[1], O::cdot(ui, y));
+        if constexpr (DMODE == 3 || DMODE == 4) {  // filter entry: m0 = <x,x>, m1 = <x,u>
+            if constexpr (DMODE == 3) st_stream(&X0[own], ui);  // x0 = X (direct moments)
+            dot_acc<O>(acc_d[0], ui, ui);
+            dot_acc<O>(acc_d[1], ui, y);
         }
     } else if constexpr (KIND == kStepStart2) {
         // w = spmmvm(A,u,2a,2b); w = 1*w + (-1)*x + 0*x; x = c0 x + c1 u + c2 w  (filter.hpp:93-103)
@@ -302,7 +379,8 @@ __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T w
         if (beta != 0.0) wr = O::vadd(wr, O::smul(beta, ui));
         const T wn = O::vadd(O::vadd(O::smul(1.0, wr), O::smul(-1.0, xi)), O::smul(0.0, xi));
         st_stream(&W[own], wn);
-        if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(xi, wn));
+        if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], xi, wn);
+        if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
         const T xn = O::vadd(O::vadd(O::smul(coeff, xi), O::smul(c1, ui)), O::smul(c2, wn));
         st_stream(&X[own], xn);
     } else {
@@ -311,11 +389,12 @@ __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T w
         st_stream(&W[own], wn);
         if constexpr (KIND == kStepFused) {
             if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
-            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+            if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
             st_stream(&X[own], O::vadd(xi, O::smul(coeff, wn)));  // kernels.hpp:106
         } else {
-            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+            if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
         }
+        if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
     }
 }
 

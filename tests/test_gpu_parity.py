@@ -133,8 +133,10 @@ PAIR_CASES = [
 @pytest.mark.parametrize("name,l,nb,deg,knobs", PAIR_CASES)
 def test_apply_filter_pair_kernel_bitexact(ctx, orc, name, l, nb, deg, knobs):
     """Two fused steps per launch (pair.cu, option pair=2): X bit-identical to the
-    oracle's apply_filter (filter.hpp:73-116), moments within 1e-12."""
+    oracle's apply_filter (filter.hpp:73-116), moments (direct <x0, w> mode, which the
+    pair kernel carries through both steps) within 1e-12."""
     ctx.set_option("pair", 2)
+    ctx.set_option("moments", "direct")
     for k, v in knobs.items():
         ctx.set_option(k, v)
     try:
@@ -154,8 +156,70 @@ def test_apply_filter_pair_kernel_bitexact(ctx, orc, name, l, nb, deg, knobs):
             assert launched == 2 + (deg - 2 + 1) // 2
     finally:
         ctx.set_option("pair", 0)
+        ctx.set_option("moments", "doubling")
         for k in knobs:
             ctx.set_option(k, -1 if k == "pair_extra" else (1 if k == "pair_hints" else 0))
+
+
+MOMENT_CASES = [("ti", (4, 4, 4), 5), ("ti", (3, 5, 4), 32), ("graphene", (16, 16), 40),
+                ("graphene", (13, 7), 1), ("graphene", (16, 16), 3)]
+
+
+@pytest.mark.parametrize("name,l,nb", MOMENT_CASES)
+@pytest.mark.parametrize("deg", [2, 3, 4, 5, 30, 101])
+@pytest.mark.parametrize("mode", ["doubling", "direct"])
+def test_apply_filter_moments_both_modes(ctx, orc, name, l, nb, deg, mode):
+    """MomentTable (filter.hpp:61-68, 86-113) by direct <x0, T_n x0> dots and by the
+    Chebyshev doubling identities (Hermitian lattices): within 1e-12 of the column norm
+    of the oracle's direct sums; X stays bit-exact."""
+    ctx.set_option("moments", mode)
+    try:
+        A, c = make_case(ctx, orc, name, l)
+        bounds = (-3.2, 3.3) if name == "graphene" else (-5.6, 5.6)
+        p = cf.make_filter((-0.25, 0.2), bounds, deg, "jackson")
+        x0 = orc.randomize(c.dim, nb, 31, name == "ti")
+        X = block(A, x0)
+        mom = cf.apply_filter(A, X, p, want_moments=True)
+        xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+        assert bits_equal(X.to_numpy(), xr)
+        assert mom.m.shape == mr.shape
+        assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
+    finally:
+        ctx.set_option("moments", "doubling")
+
+
+def test_moments_non_hermitian_operator_uses_direct_dots(ctx, orc):
+    """A from_csr operator that is not bitwise Hermitian must not use the doubling
+    identities (they would give wrong moments): moments equal the oracle's direct sums."""
+    rng = np.random.default_rng(3)
+    d = 40
+    dense = np.where(rng.random((d, d)) < 0.15, rng.uniform(-1, 1, (d, d)), 0.0)
+    np.fill_diagonal(dense, rng.uniform(-1, 1, d))
+    offs = np.concatenate([[0], np.cumsum((dense != 0).sum(1))]).astype(np.int64)
+    cols = np.nonzero(dense)[1].astype(np.int64)
+    vals = dense[dense != 0]
+    A = cf.SparseMatrix.from_csr(ctx, d, offs, cols, vals)
+    import oracle
+    c = oracle.CSR(offs, cols, vals)
+    p = cf.make_filter((-0.2, 0.2), (-4.0, 4.0), 12, "lanczos2")
+    x0 = orc.randomize(d, 3, 2)
+    X = block(A, x0)
+    mom = cf.apply_filter(A, X, p, want_moments=True)
+    xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+    assert bits_equal(X.to_numpy(), xr)
+    assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
+    # and the symmetric part of it is detected as Hermitian (doubling within tolerance)
+    sym = np.triu(dense) + np.triu(dense, 1).T
+    offs = np.concatenate([[0], np.cumsum((sym != 0).sum(1))]).astype(np.int64)
+    cols = np.nonzero(sym)[1].astype(np.int64)
+    vals = sym[sym != 0]
+    B = cf.SparseMatrix.from_csr(ctx, d, offs, cols, vals)
+    XB = block(B, x0)
+    momb = cf.apply_filter(B, XB, p, want_moments=True)
+    xr, mr = orc.apply_filter(oracle.CSR(offs, cols, vals), x0, p.combined, p.alpha, p.beta,
+                              want_moments=True)
+    assert bits_equal(XB.to_numpy(), xr)
+    assert np.max(np.abs(momb.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
 
 
 def test_apply_filter_host_e2e(ctx, orc):

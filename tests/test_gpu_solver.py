@@ -139,12 +139,19 @@ def test_kpm_flat_dos(ctx):
         cf.kpm_dos(B, (-1.0, 1.0), 2000, 4, 8)
 
 
-def test_kpm_matches_reference_moments(ctx, orc):
-    """Same probe stream as the reference -> moments agree to rounding."""
+@pytest.mark.parametrize("mode", ["doubling", "direct"])
+def test_kpm_matches_reference_moments(ctx, orc, mode):
+    """Same probe stream as the reference -> moments agree to rounding, whether each
+    moment is a <z, T_n z> dot (spectral.cpp:186-195) or comes from the doubling
+    identities over half the recurrence steps."""
     path = os.path.join(GOLDEN, "kpm_ti4.json")
     g = json.load(open(path))
-    A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(4, 4, 4, disorder=0.5, seed=3))
-    dos = cf.kpm_dos(A, g["bounds"], g["order"], g["samples"], g["seed"])
+    ctx.set_option("moments", mode)
+    try:
+        A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(4, 4, 4, disorder=0.5, seed=3))
+        dos = cf.kpm_dos(A, g["bounds"], g["order"], g["samples"], g["seed"])
+    finally:
+        ctx.set_option("moments", "doubling")
     mu = np.array(g["mu"])
     assert np.max(np.abs(dos.moments - mu)) <= 1e-9 * mu[0]
 
