@@ -62,6 +62,8 @@ class Context {
     Context& operator=(const Context&) = delete;
     chebfd_ctx* get() const { return h_; }
     void synchronize() { check(chebfd_ctx_synchronize(h_)); }
+    // CHEBFD_OPT_* (chebfd_b200.h); drops captured filter graphs
+    void set_option(int option, std::int64_t value) { check(chebfd_ctx_set_option(h_, option, value)); }
 
   private:
     chebfd_ctx* h_ = nullptr;
@@ -343,6 +345,38 @@ std::optional<MomentTable> apply_filter(const SparseMatrix<S>& A, BlockVector<S>
                               mt ? mt->m.data() : nullptr));
     return mt;
 }
+
+// apply_filter on a HOST block (row-major, this rank's rows), end to end
+template <class S>
+std::optional<MomentTable> apply_filter_host(const SparseMatrix<S>& A, std::vector<S>& x, Index width,
+                                             const FilterPolynomial& p, bool want_moments = false) {
+    std::optional<MomentTable> mt;
+    if (want_moments)
+        mt = MomentTable{p.degree, width, std::vector<double>(static_cast<size_t>((p.degree + 1) * width))};
+    check(chebfd_apply_filter_host(A.get(), x.data(), width, p.combined.data(), p.degree, p.alpha,
+                                   p.beta, mt ? mt->m.data() : nullptr));
+    return mt;
+}
+
+// A stream of host blocks filtered with the copies of neighbouring jobs overlapped
+// (chebfd_filter_pipe_*).  Buffers must outlive wait(); results = apply_filter_host's.
+template <class S>
+class FilterPipe {
+  public:
+    FilterPipe(const SparseMatrix<S>& A, Index width) { check(chebfd_filter_pipe_create(A.get(), width, &h_)); }
+    ~FilterPipe() {
+        if (h_) chebfd_filter_pipe_destroy(h_);
+    }
+    FilterPipe(const FilterPipe&) = delete;
+    FilterPipe& operator=(const FilterPipe&) = delete;
+    void submit(const S* in, S* out, const FilterPolynomial& p) {
+        check(chebfd_filter_pipe_submit(h_, in, out, p.combined.data(), p.degree, p.alpha, p.beta));
+    }
+    void wait() { check(chebfd_filter_pipe_wait(h_)); }
+
+  private:
+    chebfd_filter_pipe* h_ = nullptr;
+};
 
 // ---- solver / spectral (solver.hpp, spectral.hpp) ------------------------------------------------
 inline Interval lanczos_bounds_of(chebfd_matrix* a, int iters, std::uint64_t seed) {

@@ -4,6 +4,7 @@
 // Exit code 0 on success.
 #include <chebfd_b200.hpp>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -94,6 +95,25 @@ int main(int argc, char** argv) {
     X.save(dir + "/use_wrapper.cbfd");
     auto Y = cb::BlockVector<cb::Complex>::load(A, dir + "/use_wrapper.cbfd");
     EXPECT(Y.download() == X.download());
+    // a stream of host blocks through FilterPipe = apply_filter_host, bit for bit
+    std::vector<cb::Complex> h1 = Y.download(), h2 = h1, h3 = h1, h4(h1.size());
+    cb::apply_filter_host(A, h1, 8, pf);
+    {
+        cb::FilterPipe<cb::Complex> pipe(A, 8);
+        pipe.submit(h2.data(), h2.data(), pf);
+        pipe.submit(h3.data(), h4.data(), pf);
+        pipe.wait();
+    }
+    EXPECT(h1 == h2 && h1 == h4);
+    // moments by direct <x0, w> dots vs the doubling identities: same table to rounding
+    cb::BlockVector<cb::Complex> Z(A, 8);
+    Z.randomize(3);
+    ctx.set_option(CHEBFD_OPT_MOMENTS, 0);
+    auto md = cb::apply_filter(A, Z, pf, true);
+    ctx.set_option(CHEBFD_OPT_MOMENTS, 1);
+    double worst = 0.0;
+    for (size_t i = 0; i < md->m.size(); ++i) worst = std::max(worst, std::abs(md->m[i] - m->m[i]));
+    EXPECT(worst <= 1e-12 * std::abs(m->m[0]));
     std::printf("%s (device)\n", fails ? "FAILED" : "ok");
     return fails;
 }
