@@ -303,6 +303,7 @@ void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
         s.row1 = p.local;
         s.partial_base = 0;
         s.final_launch = true;
+        s.pdl_ok = true;  // one kernel per step, stream-ordered after the previous one
         launch_step(c, s, c.stream);
         return;
     }
@@ -761,6 +762,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->pair_mode = static_cast<int>(value);
         else if (option == CHEBFD_OPT_MOMENTS)
             c->moments_mode = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_PDL)
+            c->pdl = value != 0;
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
             c->pair_tile_rows = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_THREADS)

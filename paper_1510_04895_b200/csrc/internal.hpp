@@ -187,6 +187,9 @@ struct Context {
     // filter / KPM moments: 0 direct <x0, T_n x0> per step (x0 stream), 1 doubling from
     // <V_n, V_n>, <V_n, V_n+1> where the operator is Hermitian (default)
     int moments_mode = 1;
+    // step kernels of apply_filter / KPM launch as programmatic dependents of the previous
+    // step (their set-up overlaps its tail), single-rank operators
+    bool pdl = true;
     int pair_mode = 0, pair_tile_rows = 0, pair_threads = 0, pair_extra = -1, pair_hints = 1,
         pair_slab = 0;
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
@@ -240,6 +243,7 @@ struct StepArgs {
     int partial_base;        // first partial slot of this launch
     bool final_launch;       // this launch reduces all partials [0, partial_base + grid)
     int* grid_used;          // out: number of blocks used
+    bool pdl_ok;             // may launch as a programmatic dependent of the previous kernel
 };
 void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st);
 // column-slab launches launch_step will use for s (an upper bound: >= the real count)

@@ -275,10 +275,16 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
     }
     __syncthreads();
     int64_t tile = blockIdx.x;
+    // programmatic dependent launch: the launch and the set-up above overlap the previous
+    // kernel's tail; nothing in global memory is read before that grid has completed and
+    // flushed (its output may be this step's operand, or freshly scaled matrix values).
+    // A no-op when launched without the PDL attribute.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (t == 0 && tile < ntiles) issue(tile, 0);
     unsigned phases = 0u;  // bit b = parity of buffer b's next completion
     for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
         const int buf = k & 1;
+        if (tile + gridDim.x >= ntiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         if (t == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
         const int64_t c0 = cbeg + tile * NCH;
         const int64_t c1e = min(c0 + NCH, cend);
@@ -540,10 +546,13 @@ __global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
     }
     __syncthreads();
     int64_t tile = blockIdx.x;
+    // programmatic dependent launch: W / X tiles (TMA) are the previous step's output
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (t == 0 && tile < ntiles) issue(tile, 0);
     unsigned phases = 0u;
     for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
         const int buf = k & 1;
+        if (tile + gridDim.x >= ntiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         if (t == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
         const int64_t c = cbeg + tile;
         const int64_t sbase = cptr[c];
@@ -1093,6 +1102,24 @@ inline Geometry geometry_pow2(int units, int cap = CFD_TMA_THREADS) {
     return g;
 }
 
+// Launch a step kernel, as a programmatic dependent of the previous kernel on the stream
+// when `pdl` (the kernel calls griddepcontrol.wait before touching block vectors).
+template <class K>
+void launch_step_kernel(K kernel, int grid, int threads, size_t smem, cudaStream_t st, bool pdl,
+                        const StepParams& p) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CFD_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
+}
+
 template <class K>
 int max_blocks_for(K kernel, int threads, size_t smem, int num_sms) {
     int per_sm = 0;
@@ -1250,7 +1277,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
             p.nparts = s.partial_base + grid;
             p.final_launch = s.final_launch ? 1 : 0;
             p.counter = ctx.counter.as<unsigned>();
-            k2<<<grid, 256, smem, st>>>(p);
+            launch_step_kernel(k2, grid, 256, smem, st,
+                               ctx.pdl && s.pdl_ok && nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms), p);
             CFD_CUDA(cudaGetLastError());
             ctx.launches++;
             if (s.grid_used) *s.grid_used = grid;
@@ -1334,7 +1362,10 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         p.counter = ctx.counter.as<unsigned>();
         p.tr = TR;
         if (nrows > 0) {
-            kernel<<<grid, g.threads, smem, st>>>(p);
+            // PDL pays where launches dominate (C1: 4.2 -> 3.6 us per step); on operators of
+            // 4 x SMs tiles or more it measured neutral to -2 % (C2, C5), so only there
+            const bool pdl = tma && ctx.pdl && s.pdl_ok && nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms);
+            launch_step_kernel(kernel, grid, g.threads, smem, st, pdl, p);
             CFD_CUDA(cudaGetLastError());
             ctx.launches++;
         }
