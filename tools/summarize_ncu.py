@@ -35,10 +35,13 @@ def launches(path):
     ki = hdr.index("Kernel Name")
     vi = hdr.index("Metric Value")
     ui = hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
     per = collections.defaultdict(list)
     for r in rows[1:]:
         if len(r) <= vi:
             continue
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue  # launch lists captured with extra metrics: durations only
         v = float(r[vi].replace(",", ""))
         if r[ui] == "ms":
             v *= 1e3
