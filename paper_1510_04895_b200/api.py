@@ -634,6 +634,13 @@ class FilterPipe:
         if self._h:
             _check(_lib().chebfd_filter_pipe_destroy(self._h))
             self._h = None
+        self._keep.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def host_array(shape, dtype):
