@@ -156,6 +156,21 @@ def test_kpm_matches_reference_moments(ctx, orc, mode):
     assert np.max(np.abs(dos.moments - mu)) <= 1e-9 * mu[0]
 
 
+@pytest.mark.parametrize("order", [2, 3, 40, 41, 257])
+def test_kpm_doubling_equals_direct(ctx, order):
+    """kpm_dos moments from the doubling identities (order/2 + 1 recurrence steps) equal the
+    direct <z, T_n z> moments (spectral.cpp:186-195) to rounding, odd and even orders."""
+    A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(5, 4, 6, disorder=0.5, seed=2))
+    b = (-6.0, 6.0)
+    out = {}
+    for mode in ("direct", "doubling"):
+        ctx.set_option("moments", mode)
+        out[mode] = cf.kpm_dos(A, b, order, 8, 3).moments
+    ctx.set_option("moments", "doubling")
+    assert out["direct"].shape == out["doubling"].shape == (order + 1,)
+    assert np.max(np.abs(out["direct"] - out["doubling"])) <= 1e-11 * A.dim()
+
+
 def test_solve_random_matrix_interior(ctx):
     """test_solver.cpp:147-192"""
     d = 200
