@@ -97,10 +97,10 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_SLAB_UNITS = 5, CHEBFD_OPT_PAIR = 6, CHEBFD_OPT_PAIR_TILE_ROWS = 7,
        CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
        CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12, CHEBFD_OPT_PDL = 14 };
-/* CHEBFD_OPT_PDL (default 1): on small single-rank operators (fewer than 4 x SMs row
- * tiles, where launches dominate) the step kernels launch as programmatic dependents of
- * the previous kernel (griddepcontrol), so each step's launch and set-up overlap the
- * previous step's tail. */
+/* CHEBFD_OPT_PDL: step kernels launch as programmatic dependents of the previous
+ * kernel (griddepcontrol), so each step's launch and set-up overlap the previous step's
+ * tail -- 1 (default) on small single-rank operators (fewer than 4 x SMs row tiles,
+ * where launches dominate), 2 on every single-rank operator, 0 never. */
 /* CHEBFD_OPT_MOMENTS: how apply_filter and kpm_dos form <x0, T_n(h) x0>: 0 one
  * dot product against the kept x0 per step (the reference's way, filter.hpp:86-113,
  * spectral.cpp:186-195); 1 (default) where the operator is bitwise Hermitian, the

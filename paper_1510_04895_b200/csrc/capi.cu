@@ -763,7 +763,7 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
         else if (option == CHEBFD_OPT_MOMENTS)
             c->moments_mode = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PDL)
-            c->pdl = value != 0;
+            c->pdl = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
             c->pair_tile_rows = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_THREADS)

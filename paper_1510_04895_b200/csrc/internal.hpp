@@ -189,7 +189,7 @@ struct Context {
     int moments_mode = 1;
     // step kernels of apply_filter / KPM launch as programmatic dependents of the previous
     // step (their set-up overlaps its tail), single-rank operators
-    bool pdl = true;
+    int pdl = 1;  // 0 off, 1 small operators (launch-bound), 2 every single-rank step
     int pair_mode = 0, pair_tile_rows = 0, pair_threads = 0, pair_extra = -1, pair_hints = 1,
         pair_slab = 0;
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)

@@ -1278,7 +1278,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
             p.final_launch = s.final_launch ? 1 : 0;
             p.counter = ctx.counter.as<unsigned>();
             launch_step_kernel(k2, grid, 256, smem, st,
-                               ctx.pdl && s.pdl_ok && nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms), p);
+                               s.pdl_ok && (ctx.pdl == 2 || (ctx.pdl == 1 && nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms))),
+                               p);
             CFD_CUDA(cudaGetLastError());
             ctx.launches++;
             if (s.grid_used) *s.grid_used = grid;
@@ -1364,7 +1365,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         if (nrows > 0) {
             // PDL pays where launches dominate (C1: 4.2 -> 3.6 us per step); on operators of
             // 4 x SMs tiles or more it measured neutral to -2 % (C2, C5), so only there
-            const bool pdl = tma && ctx.pdl && s.pdl_ok && nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms);
+            const bool pdl = tma && s.pdl_ok &&
+                             (ctx.pdl == 2 || (ctx.pdl == 1 && nrows / 64 < 4 * static_cast<int64_t>(ctx.num_sms)));
             launch_step_kernel(kernel, grid, g.threads, smem, st, pdl, p);
             CFD_CUDA(cudaGetLastError());
             ctx.launches++;
