@@ -161,7 +161,7 @@ class Context:
         ("direct" | "doubling": how filter / KPM moments are formed)."""
         code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5, "pair": 6,
                 "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
-                "pair_slab": 11, "moments": 12, "pdl": 14}[name]
+                "pair_slab": 11, "moments": 12, "pdl": 14, "delayed_x": 15}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):

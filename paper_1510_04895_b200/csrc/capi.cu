@@ -511,10 +511,14 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     run_step_all(c, a, s2, *ws.u);
     Block* pu = ws.u.get();
     Block* pw = ws.w.get();
+    // delayed X update (CHEBFD_OPT_DELAYED_X): of each pair of steps the first runs without
+    // touching X (kStepRecur) and the second adds both steps' terms in the reference's order
+    // (kStepFusedX2), so X is read and written every second step -- same bits
+    bool x_pending = false;
     for (int n = 3; n <= degree; ++n) {
         std::swap(pu, pw);  // swap handles, never copies
         const bool dots_n = moments && (!dbl || 2 * n - 2 <= degree);
-        if (n < degree && !(dbl && dots_n) &&
+        if (!x_pending && n < degree && !(dbl && dots_n) &&
             run_pair_step(c, a, *pu, *pw, x, alpha, beta, coeff_dev, n,
                           dots_n ? ws.x0->owned() : nullptr,
                           dots_n ? mom_dev + static_cast<int64_t>(n) * nb : nullptr)) {
@@ -524,7 +528,15 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
             continue;
         }
         StepArgs f{};
-        f.kind_step = kStepFused;
+        if (x_pending) {
+            f.kind_step = kStepFusedX2;  // X += c_{n-1} V_{n-1}; X += c_n V_n
+            x_pending = false;
+        } else if (c.delayed_x && n < degree) {
+            f.kind_step = kStepRecur;  // V_n only; its X term rides on step n + 1
+            x_pending = true;
+        } else {
+            f.kind_step = kStepFused;
+        }
         f.w = pw->owned();
         f.x = x.owned();
         f.x0 = dots_n && !dbl ? ws.x0->owned() : nullptr;
@@ -764,6 +776,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->moments_mode = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PDL)
             c->pdl = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_DELAYED_X)
+            c->delayed_x = value != 0;
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
             c->pair_tile_rows = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_THREADS)

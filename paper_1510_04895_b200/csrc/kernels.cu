@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
     const M* __restrict__ vals = static_cast<const M*>(p.vals);
     const int* __restrict__ cols = p.cols;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
-    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -83,8 +84,8 @@ __global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
         const int64_t own = r * p.pitch + col_off;
         // own-row streams first: independent of the gathers, so they overlap
         T wi{}, xi{}, x0v{};
-        if constexpr (KIND == kStepFused || KIND == kStepRecur) wi = ld_stream(&W[own]);
-        if constexpr (KIND == kStepFused || KIND == kStepStart2) xi = ld_stream(&X[own]);
+        if constexpr (kind_reads_w(KIND)) wi = ld_stream(&W[own]);
+        if constexpr (kind_reads_x(KIND)) xi = ld_stream(&X[own]);
         if constexpr (DMODE == 2 && KIND != kStepStart2) x0v = ld_stream(&X0[own]);
         const int64_t chunk = r >> 5;
         const int lane = static_cast<int>(r & 31);
@@ -161,7 +162,8 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
     const int pitch = p.pitch;
     const int64_t halo = p.halo_lo;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
-    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -223,8 +225,8 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
         auto ldg = [&](const T* q) { return ldg_pol(q, pol_keep); };
         auto ld_stream = [&](const T* q) { return lds_pol(q, pol_stream); };
 #endif
-        if constexpr (KIND == kStepFused || KIND == kStepRecur) wi = ld_stream(&W[own]);
-        if constexpr (KIND == kStepFused || KIND == kStepStart2) xi = ld_stream(&X[own]);
+        if constexpr (kind_reads_w(KIND)) wi = ld_stream(&W[own]);
+        if constexpr (kind_reads_x(KIND)) xi = ld_stream(&X[own]);
         if constexpr (DMODE == 2 && KIND != kStepStart2) x0v = ld_stream(&X0[own]);
         T acc = O::zero();
         if constexpr (FAST) {
@@ -390,6 +392,9 @@ __device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, c
             if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
             if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
             x_out = O::vadd(xi, O::smul(coeff, wn));
+        } else if constexpr (KIND == kStepFusedX2) {
+            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+            x_out = O::vadd(O::vadd(xi, O::smul(c1, ui)), O::smul(coeff, wn));
         } else {
             if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
         }
@@ -404,8 +409,8 @@ __global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
     using M = typename O::M;
     using P = U2<T>;
     constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
-    constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
-    constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
+    constexpr bool HAS_W = kind_reads_w(KIND);
+    constexpr bool HAS_X = kind_reads_x(KIND);
     constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
     constexpr int NS = (HAS_W ? 1 : 0) + (HAS_X ? 1 : 0) + (HAS_X0 ? 1 : 0);  // staged streams
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -438,7 +443,8 @@ __global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
     const M* __restrict__ gvals = static_cast<const M*>(p.svals);
     const int64_t halo = p.halo_lo;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
-    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
         const int64_t own = r * pitch + cu;
         st256_cs(&W[own], wo);
         if constexpr (KIND == kStepSpmmvm && DMODE == 3) st256_cs(&X0[own], x0o);
-        if constexpr (KIND == kStepFused || KIND == kStepStart2) st256_cs(&X[own], xo);
+        if constexpr (kind_reads_x(KIND)) st256_cs(&X[own], xo);
     };
 
     if (t == 0) {
@@ -613,8 +619,8 @@ __global__ void __launch_bounds__(256, 1) step_stage_kernel(const StepParams p, 
     using M = typename O::M;
     constexpr int US = 32, R = 8, NP = 4;
     constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
-    constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
-    constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
+    constexpr bool HAS_W = kind_reads_w(KIND);
+    constexpr bool HAS_X = kind_reads_x(KIND);
     constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[3];
@@ -641,7 +647,8 @@ __global__ void __launch_bounds__(256, 1) step_stage_kernel(const StepParams p, 
     const M* __restrict__ gvals = static_cast<const M*>(p.svals);
     const int pitch = p.pitch;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
-    if (KIND == kStepFused && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -1213,8 +1220,8 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         const bool pick = ctx.kernel_variant == 3 || (ctx.kernel_variant == 1 && MAXW <= 8);
         if (pick && tma && units == pitch && (units == 16 || units == 32) && nrows > 0) {
             constexpr int NDOT2 = NDOT;
-            constexpr bool HAS_W = (KIND == kStepFused || KIND == kStepRecur);
-            constexpr bool HAS_X = (KIND == kStepFused || KIND == kStepStart2);
+            constexpr bool HAS_W = kind_reads_w(KIND);
+            constexpr bool HAS_X = kind_reads_x(KIND);
             constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
             constexpr int NS = (HAS_W ? 1 : 0) + (HAS_X ? 1 : 0) + (HAS_X0 ? 1 : 0);
             using M = typename Ops<CPLX, T>::M;
@@ -1394,6 +1401,11 @@ void dispatch_kind_w(Context& ctx, const StepArgs& s, cudaStream_t st, int units
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepFused, 2, MAXW>(ctx, s, st, units, pitch);
             if (s.dots_mode == 4) return run_step<CPLX, T, kStepFused, 4, MAXW>(ctx, s, st, units, pitch);
             return run_step<CPLX, T, kStepFused, 0, MAXW>(ctx, s, st, units, pitch);
+        case kStepFusedX2:
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepFusedX2, 2, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 4) return run_step<CPLX, T, kStepFusedX2, 4, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 0) return run_step<CPLX, T, kStepFusedX2, 0, MAXW>(ctx, s, st, units, pitch);
+            break;
         case kStepRecur:
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepRecur, 2, MAXW>(ctx, s, st, units, pitch);
             if (s.dots_mode == 4) return run_step<CPLX, T, kStepRecur, 4, MAXW>(ctx, s, st, units, pitch);

@@ -147,6 +147,15 @@ __device__ __forceinline__ T ldcg_t(const T* p) {
     }
 }
 
+// ---- step kinds: which own-row streams a kind reads ----------------------------------
+__host__ __device__ constexpr bool kind_reads_w(int k) {
+    return k == kStepFused || k == kStepRecur || k == kStepFusedX2;
+}
+__host__ __device__ constexpr bool kind_reads_x(int k) {
+    return k == kStepFused || k == kStepStart2 || k == kStepFusedX2;
+}
+__host__ __device__ constexpr bool kind_fused(int k) { return k == kStepFused || k == kStepFusedX2; }
+
 // ---- fixed-order block + grid reduction of NDOT per-unit accumulators -------------
 // Threads are laid out t = rr*US + u.  Each CTA writes NDOT*US partials.  When all
 // partials come from this launch, the last CTA of every group of kReduceGroup CTAs sums
@@ -391,6 +400,11 @@ __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T w
             if constexpr (DMODE == 1) kahan_add<T>(acc_d[0], comp_d[0], O::cdot(xi, wn));
             if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
             st_stream(&X[own], O::vadd(xi, O::smul(coeff, wn)));  // kernels.hpp:106
+        } else if constexpr (KIND == kStepFusedX2) {
+            // the previous step's X += c_{n-1} V_{n-1} (ui) and this step's X += c_n V_n,
+            // in that order: the reference's two roundings (kernels.hpp:106, twice)
+            if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
+            st_stream(&X[own], O::vadd(O::vadd(xi, O::smul(c1, ui)), O::smul(coeff, wn)));
         } else {
             if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
         }
