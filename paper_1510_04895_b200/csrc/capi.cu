@@ -517,8 +517,9 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     bool x_pending = false;
     for (int n = 3; n <= degree; ++n) {
         std::swap(pu, pw);  // swap handles, never copies
-        const bool dots_n = moments && (!dbl || 2 * n - 2 <= degree);
-        if (!x_pending && n < degree && !(dbl && dots_n) &&
+        // the (opt-in) pair kernel carries direct <x0, w> moments only
+        const bool dots_n = moments && !dbl;
+        if (!x_pending && n < degree && !(moments && dbl && 2 * n - 3 <= degree) &&
             run_pair_step(c, a, *pu, *pw, x, alpha, beta, coeff_dev, n,
                           dots_n ? ws.x0->owned() : nullptr,
                           dots_n ? mom_dev + static_cast<int64_t>(n) * nb : nullptr)) {
@@ -528,24 +529,40 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
             continue;
         }
         StepArgs f{};
+        // moments: direct <x0, V_n> in every step; doubling: a V_n-only step holds
+        // V_{n-2}, V_{n-1}, V_n and yields moments 2n-3 .. 2n (mode 5), so the X-update
+        // steps reduce nothing; a plain fused step yields 2n-2, 2n-1 (mode 4)
+        int dmode = 0;
+        int64_t mrow = n;
         if (x_pending) {
             f.kind_step = kStepFusedX2;  // X += c_{n-1} V_{n-1}; X += c_n V_n
             x_pending = false;
+            if (moments && !dbl) dmode = 2;
         } else if (c.delayed_x && n < degree) {
             f.kind_step = kStepRecur;  // V_n only; its X term rides on step n + 1
             x_pending = true;
+            if (moments && !dbl) dmode = 2;
+            if (dbl && 2 * n - 3 <= degree) {
+                dmode = 5;
+                mrow = 2 * n - 3;
+            }
         } else {
             f.kind_step = kStepFused;
+            if (moments && !dbl) dmode = 2;
+            if (dbl && 2 * n - 2 <= degree) {
+                dmode = 4;
+                mrow = 2 * n - 2;
+            }
         }
         f.w = pw->owned();
         f.x = x.owned();
-        f.x0 = dots_n && !dbl ? ws.x0->owned() : nullptr;
+        f.x0 = dmode == 2 ? ws.x0->owned() : nullptr;
         f.alpha = 2.0 * alpha;  // kernel multiplies values by (2 alpha) as kernels.hpp:95
         f.beta = 2.0 * beta;
         f.coeff_dev = coeff_dev;
         f.coeff_index = n;
-        f.dots_mode = dots_n ? (dbl ? 4 : 2) : 0;
-        f.dots_out = dots_n ? mom_dev + static_cast<int64_t>(dbl ? 2 * n - 2 : n) * nb : nullptr;
+        f.dots_mode = dmode;
+        f.dots_out = dmode ? mom_dev + mrow * nb : nullptr;
         run_step_all(c, a, f, *pu);
     }
     if (moments) allreduce_sum(c, mom_dev, static_cast<size_t>((degree + 1) * nb), c.stream);
@@ -573,8 +590,8 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
     std::memcpy(&key.beta_bits, &beta, 8);
     const size_t coeff_bytes = sizeof(double) * (degree + 1);
     const size_t mom_bytes = sizeof(double) * (degree + 1) * std::max<int64_t>(nb, 1);
-    // doubling writes raw sums of moment pairs: up to two rows past the table
-    const size_t mom_alloc = mom_bytes + (dbl ? 2 * sizeof(double) * std::max<int64_t>(nb, 1) : 0);
+    // doubling writes raw sums of 2 or 4 consecutive moments: up to three rows past the table
+    const size_t mom_alloc = mom_bytes + (dbl ? 3 * sizeof(double) * std::max<int64_t>(nb, 1) : 0);
     auto finish_moments = [&] {
         if (dbl) moments_from_doubling(moments_host, degree + 1, nb);
     };

@@ -47,7 +47,7 @@ template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 __global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
+    constexpr int NDOT = dots_of(DMODE);
     const int t = threadIdx.x;
     const int rr = t / p.US;
     const int u = t - rr * p.US;
@@ -131,7 +131,7 @@ template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
+    constexpr int NDOT = dots_of(DMODE);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[2];
     const int t = threadIdx.x;
@@ -399,6 +399,7 @@ __device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, c
             if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
         }
         if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
+        if constexpr (DMODE == 5) moment_quad<O>(acc_d, wi, ui, wn);
     }
 }
 
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
     using O = Ops<CPLX, T>;
     using M = typename O::M;
     using P = U2<T>;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
+    constexpr int NDOT = dots_of(DMODE);
     constexpr bool HAS_W = kind_reads_w(KIND);
     constexpr bool HAS_X = kind_reads_x(KIND);
     constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(256, 1) step_stage_kernel(const StepParams p, 
     using O = Ops<CPLX, T>;
     using M = typename O::M;
     constexpr int US = 32, R = 8, NP = 4;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
+    constexpr int NDOT = dots_of(DMODE);
     constexpr bool HAS_W = kind_reads_w(KIND);
     constexpr bool HAS_X = kind_reads_x(KIND);
     constexpr bool HAS_X0 = (DMODE == 2 && KIND != kStepStart2);
@@ -1137,7 +1138,7 @@ int max_blocks_for(K kernel, int threads, size_t smem, int num_sms) {
 template <bool CPLX, class T, int KIND, int DMODE, int MAXW>
 void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
     const Matrix& a = *s.a;
-    constexpr int NDOT = (DMODE == 0) ? 0 : (DMODE >= 3 ? 2 : 1);
+    constexpr int NDOT = dots_of(DMODE);
     const int64_t nrows = s.row1 - s.row0;
     constexpr int MW = MAXW > 0 ? MAXW : 4;
     const void* svals = s.alpha == 1.0 ? a.vals.p : find_scaled(a, s.alpha);
@@ -1145,7 +1146,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     auto kernel = tma ? step_tma_kernel<CPLX, T, KIND, DMODE, MW>
                       : step_kernel<CPLX, T, KIND, DMODE, 0>;
     int used_total = 0;
-    if constexpr (MAXW >= 8 && std::is_same_v<T, double2> && DMODE != 4) {
+    if constexpr (MAXW >= 8 && std::is_same_v<T, double2> && DMODE < 4) {
         // staged-gather kernel: one 512-byte row slot, plan present and fitting shared memory
         if (ctx.kernel_variant == 2 && tma && units == 32 && pitch == 32 && a.stage_max_rows > 0 &&
             nrows > 0) {
@@ -1409,6 +1410,7 @@ void dispatch_kind_w(Context& ctx, const StepArgs& s, cudaStream_t st, int units
         case kStepRecur:
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepRecur, 2, MAXW>(ctx, s, st, units, pitch);
             if (s.dots_mode == 4) return run_step<CPLX, T, kStepRecur, 4, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 5) return run_step<CPLX, T, kStepRecur, 5, MAXW>(ctx, s, st, units, pitch);
             return run_step<CPLX, T, kStepRecur, 0, MAXW>(ctx, s, st, units, pitch);
     }
     fail(CHEBFD_ERR_INVALID_ARGUMENT, "bad step kind");

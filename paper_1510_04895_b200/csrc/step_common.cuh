@@ -147,6 +147,12 @@ __device__ __forceinline__ T ldcg_t(const T* p) {
     }
 }
 
+// dot products a step accumulates: 1 Kahan <x,w> / 2 <x0,w> / 3 m0,m1 + x0 copy /
+// 4 moment pair / 5 moment quad (doubling identities)
+__host__ __device__ constexpr int dots_of(int dmode) {
+    return dmode == 0 ? 0 : (dmode == 5 ? 4 : (dmode >= 3 ? 2 : 1));
+}
+
 // ---- step kinds: which own-row streams a kind reads ----------------------------------
 __host__ __device__ constexpr bool kind_reads_w(int k) {
     return k == kStepFused || k == kStepRecur || k == kStepFusedX2;
@@ -367,6 +373,18 @@ __device__ __forceinline__ void moment_pair(A (&acc_d)[NA], const T ui, const T 
     dot_acc<O>(acc_d[1], ui, wn);
 }
 
+// Four moments from one recurrence step (DMODE 5): the step producing V_n holds V_{n-2}
+// (wi), V_{n-1} (ui) and V_n (wn) in registers, whose products give the raw sums of
+// moments 2n-3 (<V_{n-2},V_{n-1}>), 2n-2, 2n-1 and 2n (<V_n,V_n>).  With the delayed X
+// update every second step is such a V_n-only step, so the X-update steps reduce nothing.
+template <class O, class A, class T, int NA>
+__device__ __forceinline__ void moment_quad(A (&acc_d)[NA], const T wi, const T ui, const T wn) {
+    dot_acc<O>(acc_d[0], wi, ui);
+    dot_acc<O>(acc_d[1], ui, ui);
+    dot_acc<O>(acc_d[2], ui, wn);
+    dot_acc<O>(acc_d[3], wn, wn);
+}
+
 template <class O, class T, int KIND, int DMODE, class A, int NA>
 __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T wi, const T xi,
                                               const T x0v, int64_t own, T* __restrict__ W,
@@ -409,6 +427,7 @@ __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T w
             if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
         }
         if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
+        if constexpr (DMODE == 5) moment_quad<O>(acc_d, wi, ui, wn);
     }
 }
 
