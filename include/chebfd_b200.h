@@ -98,10 +98,11 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
        CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12, CHEBFD_OPT_PDL = 14,
        CHEBFD_OPT_DELAYED_X = 15 };
-/* CHEBFD_OPT_DELAYED_X (default 1): apply_filter's fused loop updates X every second
- * step -- the first step of each pair computes V_n only, the second adds
- * c_{n-1} V_{n-1} then c_n V_n to X, the reference's two roundings in its order
- * (kernels.hpp:106) -- so X streams once per two steps; results are bit-identical. */
+/* CHEBFD_OPT_DELAYED_X (default 3): apply_filter's fused loop updates X once per G
+ * steps (G = 2 or 3; 0 / 1: every step) -- the first G-1 steps of a group compute V_n
+ * only, the last adds c_{n-2} V_{n-2}, c_{n-1} V_{n-1}, c_n V_n to X, the reference's
+ * roundings in its order (kernels.hpp:106) -- so X streams once per G steps; results
+ * are bit-identical. */
 /* CHEBFD_OPT_PDL: step kernels launch as programmatic dependents of the previous
  * kernel (griddepcontrol), so each step's launch and set-up overlap the previous step's
  * tail -- 1 (default) on small single-rank operators (fewer than 4 x SMs row tiles,

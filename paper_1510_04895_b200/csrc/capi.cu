@@ -511,12 +511,16 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     run_step_all(c, a, s2, *ws.u);
     Block* pu = ws.u.get();
     Block* pw = ws.w.get();
-    // delayed X update (CHEBFD_OPT_DELAYED_X): of each pair of steps the first runs without
-    // touching X (kStepRecur) and the second adds both steps' terms in the reference's order
-    // (kStepFusedX2), so X is read and written every second step -- same bits
-    bool x_pending = false;
+    // delayed X update (CHEBFD_OPT_DELAYED_X = G): of each group of G steps the first G-1 run
+    // without touching X (kStepRecur) and the last adds all their terms in the reference's
+    // order (kStepFusedX2 / X3: the V's of the group are its registers' wi, ui, wn), so X is
+    // read and written once per G steps -- same bits
+    const int group = std::clamp(c.delayed_x, 1, 3);
+    int grp_pos = 0, grp_len = 1;
     for (int n = 3; n <= degree; ++n) {
         std::swap(pu, pw);  // swap handles, never copies
+        if (grp_pos == 0) grp_len = std::min(group, degree - n + 1);
+        const bool x_pending = grp_pos > 0;
         // the (opt-in) pair kernel carries direct <x0, w> moments only
         const bool dots_n = moments && !dbl;
         if (!x_pending && n < degree && !(moments && dbl && 2 * n - 3 <= degree) &&
@@ -534,18 +538,22 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
         // steps reduce nothing; a plain fused step yields 2n-2, 2n-1 (mode 4)
         int dmode = 0;
         int64_t mrow = n;
-        if (x_pending) {
-            f.kind_step = kStepFusedX2;  // X += c_{n-1} V_{n-1}; X += c_n V_n
-            x_pending = false;
+        if (grp_len > 1 && grp_pos == grp_len - 1) {
+            // X += c_{n-2} V_{n-2} (X3 only), c_{n-1} V_{n-1}, c_n V_n
+            f.kind_step = grp_len == 3 ? kStepFusedX3 : kStepFusedX2;
+            grp_pos = 0;
             if (moments && !dbl) dmode = 2;
-        } else if (c.delayed_x && n < degree) {
-            f.kind_step = kStepRecur;  // V_n only; its X term rides on step n + 1
-            x_pending = true;
+        } else if (grp_len > 1) {
+            f.kind_step = kStepRecur;  // V_n only; its X term rides on the group's last step
             if (moments && !dbl) dmode = 2;
-            if (dbl && 2 * n - 3 <= degree) {
-                dmode = 5;
+            if (dbl && grp_pos == 0 && 2 * n - 3 <= degree) {
+                dmode = 5;  // moments 2n-3 .. 2n
                 mrow = 2 * n - 3;
+            } else if (dbl && grp_pos == 1 && 2 * n - 1 <= degree) {
+                dmode = 6;  // the second V_n-only step of a triple adds 2n-1, 2n
+                mrow = 2 * n - 1;
             }
+            ++grp_pos;
         } else {
             f.kind_step = kStepFused;
             if (moments && !dbl) dmode = 2;
@@ -794,7 +802,7 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
         else if (option == CHEBFD_OPT_PDL)
             c->pdl = static_cast<int>(value);
         else if (option == CHEBFD_OPT_DELAYED_X)
-            c->delayed_x = value != 0;
+            c->delayed_x = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
             c->pair_tile_rows = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_THREADS)

@@ -190,8 +190,9 @@ struct Context {
     // step kernels of apply_filter / KPM launch as programmatic dependents of the previous
     // step (their set-up overlaps its tail), single-rank operators
     int pdl = 1;  // 0 off, 1 small operators (launch-bound), 2 every single-rank step
-    // apply_filter: X read and written every second step (kStepRecur + kStepFusedX2)
-    bool delayed_x = true;
+    // apply_filter: X read and written every delayed_x-th step (kStepRecur steps, then
+    // kStepFusedX2 / X3 adding their terms); 0 or 1: every step
+    int delayed_x = 3;
     int pair_mode = 0, pair_tile_rows = 0, pair_threads = 0, pair_extra = -1, pair_hints = 1,
         pair_slab = 0;
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
@@ -227,6 +228,8 @@ enum StepKind {
     kStepRecur = 3,    // recurrence_step (kernels.hpp:121-145)
     kStepFusedX2 = 4,  // spmmvm_fused whose X update also carries the previous step's:
                        // X = (X + c_{n-1} V_{n-1}) + c_n V_n (the previous step ran as kStepRecur)
+    kStepFusedX3 = 5,  // ... the previous two steps': X = ((X + c_{n-2} V_{n-2}) + c_{n-1} V_{n-1})
+                       // + c_n V_n (both ran as kStepRecur)
 };
 
 struct StepArgs {

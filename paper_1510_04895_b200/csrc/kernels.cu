@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(256, 2) step_kernel(const StepParams p) {
     const int* __restrict__ cols = p.cols;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
     if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
-    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if ((KIND == kStepFusedX2 || KIND == kStepFusedX3) && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if (KIND == kStepFusedX3 && p.coeff_dev) c2 = p.coeff_dev[p.coeff_index - 2];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -163,7 +164,8 @@ __global__ void __launch_bounds__(CFD_TMA_THREADS, CFD_TMA_MINB) step_tma_kernel
     const int64_t halo = p.halo_lo;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
     if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
-    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if ((KIND == kStepFusedX2 || KIND == kStepFusedX3) && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if (KIND == kStepFusedX3 && p.coeff_dev) c2 = p.coeff_dev[p.coeff_index - 2];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -395,11 +397,18 @@ __device__ __forceinline__ void epilogue2(const T acc, const T ui, const T wi, c
         } else if constexpr (KIND == kStepFusedX2) {
             if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
             x_out = O::vadd(O::vadd(xi, O::smul(c1, ui)), O::smul(coeff, wn));
+        } else if constexpr (KIND == kStepFusedX3) {
+            if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
+            x_out = O::vadd(O::vadd(O::vadd(xi, O::smul(c2, wi)), O::smul(c1, ui)), O::smul(coeff, wn));
         } else {
             if constexpr (DMODE == 2) acc_d[0] = O::vadd(acc_d[0], O::cdot(x0v, wn));
         }
         if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
         if constexpr (DMODE == 5) moment_quad<O>(acc_d, wi, ui, wn);
+        if constexpr (DMODE == 6) {
+            acc_d[0] = O::vadd(acc_d[0], O::cdot(ui, wn));
+            acc_d[1] = O::vadd(acc_d[1], O::cdot(wn, wn));
+        }
     }
 }
 
@@ -445,7 +454,8 @@ __global__ void __launch_bounds__(256, 2) step_tma2_kernel(const StepParams p) {
     const int64_t halo = p.halo_lo;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
     if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
-    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if ((KIND == kStepFusedX2 || KIND == kStepFusedX3) && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if (KIND == kStepFusedX3 && p.coeff_dev) c2 = p.coeff_dev[p.coeff_index - 2];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -649,7 +659,8 @@ __global__ void __launch_bounds__(256, 1) step_stage_kernel(const StepParams p, 
     const int pitch = p.pitch;
     double coeff = p.c0, c1 = p.c1, c2 = p.c2;
     if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
-    if (KIND == kStepFusedX2 && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if ((KIND == kStepFusedX2 || KIND == kStepFusedX3) && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+    if (KIND == kStepFusedX3 && p.coeff_dev) c2 = p.coeff_dev[p.coeff_index - 2];
     if (KIND == kStepStart2 && p.coeff_dev) {
         coeff = p.coeff_dev[0];
         c1 = p.coeff_dev[1];
@@ -1404,13 +1415,17 @@ void dispatch_kind_w(Context& ctx, const StepArgs& s, cudaStream_t st, int units
             return run_step<CPLX, T, kStepFused, 0, MAXW>(ctx, s, st, units, pitch);
         case kStepFusedX2:
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepFusedX2, 2, MAXW>(ctx, s, st, units, pitch);
-            if (s.dots_mode == 4) return run_step<CPLX, T, kStepFusedX2, 4, MAXW>(ctx, s, st, units, pitch);
             if (s.dots_mode == 0) return run_step<CPLX, T, kStepFusedX2, 0, MAXW>(ctx, s, st, units, pitch);
+            break;
+        case kStepFusedX3:
+            if (s.dots_mode == 2) return run_step<CPLX, T, kStepFusedX3, 2, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 0) return run_step<CPLX, T, kStepFusedX3, 0, MAXW>(ctx, s, st, units, pitch);
             break;
         case kStepRecur:
             if (s.dots_mode == 2) return run_step<CPLX, T, kStepRecur, 2, MAXW>(ctx, s, st, units, pitch);
             if (s.dots_mode == 4) return run_step<CPLX, T, kStepRecur, 4, MAXW>(ctx, s, st, units, pitch);
             if (s.dots_mode == 5) return run_step<CPLX, T, kStepRecur, 5, MAXW>(ctx, s, st, units, pitch);
+            if (s.dots_mode == 6) return run_step<CPLX, T, kStepRecur, 6, MAXW>(ctx, s, st, units, pitch);
             return run_step<CPLX, T, kStepRecur, 0, MAXW>(ctx, s, st, units, pitch);
     }
     fail(CHEBFD_ERR_INVALID_ARGUMENT, "bad step kind");

@@ -148,19 +148,21 @@ __device__ __forceinline__ T ldcg_t(const T* p) {
 }
 
 // dot products a step accumulates: 1 Kahan <x,w> / 2 <x0,w> / 3 m0,m1 + x0 copy /
-// 4 moment pair / 5 moment quad (doubling identities)
+// 4 moment pair / 5 moment quad / 6 the quad's upper pair (doubling identities)
 __host__ __device__ constexpr int dots_of(int dmode) {
     return dmode == 0 ? 0 : (dmode == 5 ? 4 : (dmode >= 3 ? 2 : 1));
 }
 
 // ---- step kinds: which own-row streams a kind reads ----------------------------------
 __host__ __device__ constexpr bool kind_reads_w(int k) {
-    return k == kStepFused || k == kStepRecur || k == kStepFusedX2;
+    return k == kStepFused || k == kStepRecur || k == kStepFusedX2 || k == kStepFusedX3;
 }
 __host__ __device__ constexpr bool kind_reads_x(int k) {
-    return k == kStepFused || k == kStepStart2 || k == kStepFusedX2;
+    return k == kStepFused || k == kStepStart2 || k == kStepFusedX2 || k == kStepFusedX3;
 }
-__host__ __device__ constexpr bool kind_fused(int k) { return k == kStepFused || k == kStepFusedX2; }
+__host__ __device__ constexpr bool kind_fused(int k) {
+    return k == kStepFused || k == kStepFusedX2 || k == kStepFusedX3;
+}
 
 // ---- fixed-order block + grid reduction of NDOT per-unit accumulators -------------
 // Threads are laid out t = rr*US + u.  Each CTA writes NDOT*US partials.  When all
@@ -423,11 +425,20 @@ __device__ __forceinline__ void step_epilogue(const T acc, const T ui, const T w
             // in that order: the reference's two roundings (kernels.hpp:106, twice)
             if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
             st_stream(&X[own], O::vadd(O::vadd(xi, O::smul(c1, ui)), O::smul(coeff, wn)));
+        } else if constexpr (KIND == kStepFusedX3) {
+            // X += c_{n-2} V_{n-2} (wi), c_{n-1} V_{n-1} (ui), c_n V_n, in that order
+            if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
+            st_stream(&X[own], O::vadd(O::vadd(O::vadd(xi, O::smul(c2, wi)), O::smul(c1, ui)),
+                                       O::smul(coeff, wn)));
         } else {
             if constexpr (DMODE == 2) dot_acc<O>(acc_d[0], x0v, wn);
         }
         if constexpr (DMODE == 4) moment_pair<O>(acc_d, ui, wn);
         if constexpr (DMODE == 5) moment_quad<O>(acc_d, wi, ui, wn);
+        if constexpr (DMODE == 6) {  // the upper pair of moment_quad: moments 2n-1, 2n
+            dot_acc<O>(acc_d[0], ui, wn);
+            dot_acc<O>(acc_d[1], wn, wn);
+        }
     }
 }
 

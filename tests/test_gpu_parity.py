@@ -188,6 +188,29 @@ def test_apply_filter_moments_both_modes(ctx, orc, name, l, nb, deg, mode):
         ctx.set_option("moments", "doubling")
 
 
+@pytest.mark.parametrize("group", [0, 2, 3])
+@pytest.mark.parametrize("deg", [2, 3, 4, 5, 6, 7, 8, 31])
+@pytest.mark.parametrize("mode", ["doubling", "direct"])
+def test_apply_filter_delayed_x_groups(ctx, orc, group, deg, mode):
+    """X updated once per G steps (V_n-only steps, then one step adding the group's terms in
+    the reference's order): X bit-identical to the oracle's per-step update, moments within
+    1e-12, for every tail length (degree - 2 mod G)."""
+    ctx.set_option("delayed_x", group)
+    ctx.set_option("moments", mode)
+    try:
+        A, c = ti(ctx, orc, (4, 5, 4))
+        p = cf.make_filter((-0.25, 0.2), (-5.6, 5.6), deg, "lanczos2")
+        x0 = orc.randomize(c.dim, 6, 17, True)
+        X = block(A, x0)
+        mom = cf.apply_filter(A, X, p, want_moments=True)
+        xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+        assert bits_equal(X.to_numpy(), xr)
+        assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
+    finally:
+        ctx.set_option("delayed_x", 3)
+        ctx.set_option("moments", "doubling")
+
+
 def test_moments_non_hermitian_operator_uses_direct_dots(ctx, orc):
     """A from_csr operator that is not bitwise Hermitian must not use the doubling
     identities (they would give wrong moments): moments equal the oracle's direct sums."""

@@ -24,7 +24,7 @@ for name, mk, nb, Np, reps, bnd in cases:
     A = mk()
     p = cf.make_filter((-0.1, 0.1), bnd, Np, "lanczos2")
     X = cf.BlockVector(A, nb).randomize_device(7)
-    for dx in (0, 1, 0, 1):
+    for dx in (0, 2, 3, 0, 2, 3):
         ctx.set_option("delayed_x", dx)
         for mom in (False, True):
             cf.apply_filter(A, X, p, want_moments=mom)
@@ -38,5 +38,5 @@ for name, mk, nb, Np, reps, bnd in cases:
                               "us_per_step": round(ms / Np * 1e3, 2)}), flush=True)
     X.close()
     A.close()
-ctx.set_option("delayed_x", 1)
+ctx.set_option("delayed_x", 3)
 ctx.close()
