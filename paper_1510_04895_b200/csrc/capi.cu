@@ -515,7 +515,10 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     // without touching X (kStepRecur) and the last adds all their terms in the reference's
     // order (kStepFusedX2 / X3: the V's of the group are its registers' wi, ui, wn), so X is
     // read and written once per G steps -- same bits
-    const int group = std::clamp(c.delayed_x, 1, 3);
+    // launch-bound operators with doubling moments: pairs (fewer reducing steps per group
+    // of work; C1 with moments 3.21 ms for pairs vs 3.29 ms for triples)
+    const bool small = a.part.local / 64 < 4 * static_cast<int64_t>(c.num_sms);
+    const int group = std::clamp(dbl && small && c.delayed_x == 3 ? 2 : c.delayed_x, 1, 3);
     int grp_pos = 0, grp_len = 1;
     for (int n = 3; n <= degree; ++n) {
         std::swap(pu, pw);  // swap handles, never copies
