@@ -183,3 +183,17 @@ def test_partition_plans_cover_rows_and_pair_up():
         # open z: the end ranks have a single neighbour
         if nranks > 1:
             assert plans[0].lo_rank == -1 and plans[-1].hi_rank == -1
+
+
+def test_python_option_codes_match_header():
+    """Context.set_option's names map to the CHEBFD_OPT_* values of the C header."""
+    text = open(HEADER).read()
+    enum = {m.group(1).lower(): int(m.group(2))
+            for m in re.finditer(r"CHEBFD_OPT_([A-Z0-9_]+)\s*=\s*(\d+)", text)}
+    import inspect
+    from paper_1510_04895_b200 import api
+    src = inspect.getsource(api.Context.set_option)
+    codes = dict(re.findall(r'"([a-z_0-9]+)": (\d+)', src.split("}[name]")[0]))
+    assert codes, "no option table found"
+    for name, code in codes.items():
+        assert enum.get(name) == int(code), (name, code, enum.get(name))
