@@ -11,6 +11,7 @@
 #include <limits>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.hpp"
@@ -169,6 +170,65 @@ void randomize_upload(Context& c, Block& b, uint64_t seed) {
     }
     cudaEventDestroy(done[0]);
     cudaEventDestroy(done[1]);
+}
+
+// The same stream generated on a helper thread with its own CUDA stream and pinned
+// buffers, so a solve's start block is produced while the device runs the Lanczos bounds
+// and the KPM DOS (the block must not be touched until join()).
+AsyncRandomize::AsyncRandomize(Context& c, Block& b, uint64_t seed) {
+    const int device = c.device;
+    th_ = std::thread([this, &b, seed, device] {
+        cudaStream_t st = nullptr;
+        char* pin = nullptr;
+        cudaEvent_t done[2] = {nullptr, nullptr};
+        try {
+            CFD_CUDA(cudaSetDevice(device));
+            CFD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            const int64_t count = b.rows * b.width;
+            const size_t esz = b.kind ? 16 : 8;
+            const int64_t first = b.row_begin * b.width;
+            const int64_t kPiece = std::max<int64_t>(
+                int64_t{1} << 22,
+                std::min<int64_t>(NormalStream::parallel_piece(b.kind), (int64_t{1} << 30) / esz));
+            CFD_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pin),
+                                    2 * static_cast<size_t>(std::min(kPiece, std::max<int64_t>(count, 1))) * esz));
+            CFD_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+            CFD_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+            NormalStream ns(seed);
+            char* dev = static_cast<char*>(b.owned());
+            const int64_t piece = std::min(kPiece, std::max<int64_t>(count, 1));
+            for (int64_t off = 0, k = 0; off < count; off += piece, ++k) {
+                const int buf = static_cast<int>(k & 1);
+                const int64_t n = std::min(piece, count - off);
+                char* h = pin + buf * piece * esz;
+                if (k >= 2) CFD_CUDA(cudaEventSynchronize(done[buf]));
+                ns.emit(b.kind, first + off, n, h);
+                CFD_CUDA(cudaMemcpyAsync(dev + off * esz, h, n * esz, cudaMemcpyHostToDevice, st));
+                CFD_CUDA(cudaEventRecord(done[buf], st));
+            }
+            CFD_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            err_ = std::current_exception();
+        }
+        if (st) cudaStreamSynchronize(st);
+        for (cudaEvent_t e : done)
+            if (e) cudaEventDestroy(e);
+        if (pin) cudaFreeHost(pin);
+        if (st) cudaStreamDestroy(st);
+    });
+}
+
+void AsyncRandomize::join() {
+    if (th_.joinable()) th_.join();
+    if (err_) {
+        auto e = err_;
+        err_ = nullptr;
+        std::rethrow_exception(e);
+    }
+}
+
+AsyncRandomize::~AsyncRandomize() {
+    if (th_.joinable()) th_.join();
 }
 
 // ---------------------------------------------------------------- helpers --

@@ -1,5 +1,7 @@
 // Helpers shared by the C-ABI translation units (capi.cu, solver.cu, blas.cu).
 #pragma once
+#include <exception>
+#include <thread>
 
 #include <string>
 
@@ -37,6 +39,19 @@ std::unique_ptr<Block> make_block(Context& c, const Matrix* m, int kind, int64_t
 void check_same_shape(const Block& x, const Block& y);
 // BlockVector::randomize of this rank's rows, streamed host -> device
 void randomize_upload(Context& c, Block& b, uint64_t seed);
+// the same on a helper thread (own stream and pinned buffers); b is ready after join()
+class AsyncRandomize {
+  public:
+    AsyncRandomize(Context& c, Block& b, uint64_t seed);
+    ~AsyncRandomize();
+    AsyncRandomize(const AsyncRandomize&) = delete;
+    AsyncRandomize& operator=(const AsyncRandomize&) = delete;
+    void join();
+
+  private:
+    std::thread th_;
+    std::exception_ptr err_;
+};
 void check_conforms(const Matrix& a, const Block& x, const char* who);
 // moments by the Chebyshev doubling identities (CHEBFD_OPT_MOMENTS, Hermitian operators)
 bool moment_doubling(const Context& c, const Matrix& a);

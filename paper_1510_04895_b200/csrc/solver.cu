@@ -390,6 +390,17 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
             return std::chrono::duration<double>(clk::now() - a).count();
         };
         auto tp = clk::now();
+        // with N_S given, the start block (solver.cpp:147-154) does not depend on the DOS:
+        // generate it on a helper thread while the device runs the bounds and the KPM DOS
+        std::unique_ptr<Block> x_early;
+        std::unique_ptr<AsyncRandomize> x_job;
+        // (only for blocks whose generation takes longer than the helper's set-up: pinned
+        // buffers and a stream cost ~50 ms, a C1 block takes 6 ms synchronously)
+        if (o->n_search > 0 && A.part.local * o->n_search >= (int64_t{1} << 26)) {
+            x_early = make_block(c, &A, A.kind, A.part.local, o->n_search, false);
+            ctx_sync(c);  // the (cached) storage and its halo clear are settled on c.stream
+            x_job = std::make_unique<AsyncRandomize>(c, *x_early, o->seed + 2);
+        }
         double blo = o->bounds_lo, bhi = o->bounds_hi;
         if (!(blo < bhi)) lanczos_bounds(c, A, 30, o->seed, &blo, &bhi);
         rep->t_bounds = secs(tp);
@@ -451,8 +462,15 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
             std::max(1.0, std::ceil(rep->n_target_estimate - 3.0 * std::sqrt(rep->n_target_estimate)));
         const int64_t ns = rep->n_search;
         tp = clk::now();
-        auto x = make_block(c, &A, A.kind, A.part.local, ns, false);
-        randomize(c, *x, o->seed + 2);
+        std::unique_ptr<Block> x;
+        if (x_job && ns == x_early->width) {
+            x_job->join();
+            x = std::move(x_early);
+        } else {
+            if (x_job) x_job->join();
+            x = make_block(c, &A, A.kind, A.part.local, ns, false);
+            randomize(c, *x, o->seed + 2);
+        }
         divide_columns(c, *x, norms(c, *x));  // unit columns (solver.cpp:149-154)
         rep->t_start = secs(tp);
         Ritz ritz;
