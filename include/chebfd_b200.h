@@ -56,6 +56,11 @@ typedef struct chebfd_block chebfd_block;
 const char* chebfd_last_error(void);
 /* Library version string. */
 const char* chebfd_version(void);
+/* Build features (bit mask): CHEBFD_FEATURE_EXPERIMENTAL = the opt-in kernel variants
+ * that measured slower than the default path (CHEBFD_OPT_PAIR != 0, CHEBFD_OPT_KERNEL
+ * = 2) are compiled in; without it setting them fails with CHEBFD_ERR_UNSUPPORTED. */
+enum { CHEBFD_FEATURE_EXPERIMENTAL = 1 };
+int chebfd_build_features(void);
 
 /* ---- context --------------------------------------------------------------- */
 /* Single-GPU context on `device` (replaces the OpenMP runtime, parallel.hpp:18-54). */
@@ -97,7 +102,22 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_SLAB_UNITS = 5, CHEBFD_OPT_PAIR = 6, CHEBFD_OPT_PAIR_TILE_ROWS = 7,
        CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
        CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12, CHEBFD_OPT_PDL = 14,
-       CHEBFD_OPT_DELAYED_X = 15 };
+       CHEBFD_OPT_DELAYED_X = 15, CHEBFD_OPT_BAND_BYTES = 16, CHEBFD_OPT_ASYNC_START = 17,
+       CHEBFD_OPT_TILES_PER_CTA = 18 };
+/* CHEBFD_OPT_TILES_PER_CTA (default 2): band-ordered launches run a non-persistent grid
+ * of this many consecutive tiles per CTA, dispatched in order by the hardware (a compact
+ * wavefront; persistent CTA-strided grids drift apart and lose the band's L2 reuse);
+ * 0 = no band order. */
+/* CHEBFD_OPT_ASYNC_START (default 2^26): chebfd_solve with n_search given generates the
+ * start block (solver.cpp:147-154) on a helper thread, overlapped with the Lanczos
+ * bounds and the KPM DOS, when local rows x n_search >= this many entries (0: never).
+ * The block is the same stream either way (BlockVector::randomize, bit-identical). */
+/* CHEBFD_OPT_BAND_BYTES (default 16 MiB): dot-free step launches on TI lattice operators
+ * whose z-plane of the gathered block exceeds 4x this many bytes sweep the rows in bands
+ * of lattice lines, plane by plane inside a band (a band slice of the block is at most
+ * this size), on a non-persistent grid (CHEBFD_OPT_TILES_PER_CTA), so the z -+ 1
+ * neighbour rows are reused from L2; 0 = row order.  Results are identical (row-local
+ * arithmetic; launches with dots keep the persistent row-order grid). */
 /* CHEBFD_OPT_DELAYED_X (default 3): apply_filter's fused loop updates X once per G
  * steps (G = 2 or 3; 0 / 1: every step) -- the first G-1 steps of a group compute V_n
  * only, the last adds c_{n-2} V_{n-2}, c_{n-1} V_{n-1}, c_n V_n to X, the reference's
@@ -204,6 +224,10 @@ int chebfd_block_create(chebfd_matrix* a, int64_t width, chebfd_block** out);
 /* A free-standing block of `dim` rows (single-GPU contexts). */
 int chebfd_block_create_dim(chebfd_ctx* ctx, int kind, int64_t dim, int64_t width,
                             chebfd_block** out);
+/* A zero-filled block with the rows (and partition / halos) of `like` and `width`
+ * columns -- what the reference's BlockVector<S>(x.dim(), m) builds inside
+ * block_mult_small / svqb_orthonormalize (kernels.hpp:216-232, solver.cpp:52-58). */
+int chebfd_block_create_like(const chebfd_block* like, int64_t width, chebfd_block** out);
 int chebfd_block_destroy(chebfd_block* b);
 int chebfd_block_info(const chebfd_block* b, int* kind, int64_t* rows, int64_t* width,
                       int64_t* row_begin);
@@ -332,6 +356,12 @@ int chebfd_kpm_dos(chebfd_matrix* a, double bounds_lo, double bounds_hi, int ord
 /* Jackson-damped count integral (ChebSeriesDensity::count, spectral.cpp:46-57) */
 int chebfd_dos_count(const double* mu, int order, double bounds_lo, double bounds_hi, double lo,
                      double hi, double* out);
+/* Jackson-damped density at lambda (ChebSeriesDensity::density, spectral.cpp:31-44) */
+int chebfd_dos_density(const double* mu, int order, double bounds_lo, double bounds_hi,
+                       double lambda, double* out);
+/* weight_density (spectral.cpp:81-88): mu[n] = sum_k moments[n * width + k], n = 0..degree.
+ * Errors (invalid_argument): empty moment table. */
+int chebfd_weight_density(const double* moments, int degree, int64_t width, double* mu);
 
 /* ---- bench front end (bench.hpp / bench.cpp) ------------------------------------- */
 /* BenchPoint (bench.hpp:49-58): model flops and traffic (bench.cpp:28-34, S_i = 4)
@@ -429,6 +459,14 @@ typedef struct {
 int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* opts, chebfd_solve_report* rep,
                  int cap, double* values, double* residual_norms, int* accepted,
                  double* history, chebfd_block** vectors);
+/* chebfd_solve plus the report's weight density (ConvergenceReport::weight, solver.cpp:
+ * 158-162): weight_moments[0..degree] = weight_density(moments of the last filter).mu
+ * (spectral.cpp:81-88), *weight_len = degree + 1 (0 when collect_weight_density = 0);
+ * weight_cap < degree + 1 is CHEBFD_ERR_INVALID_ARGUMENT. */
+int chebfd_solve_ex(chebfd_matrix* a, const chebfd_solver_options* opts, chebfd_solve_report* rep,
+                    int cap, double* values, double* residual_norms, int* accepted,
+                    double* history, chebfd_block** vectors, int weight_cap,
+                    double* weight_moments, int* weight_len);
 
 #ifdef __cplusplus
 }

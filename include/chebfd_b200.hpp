@@ -183,9 +183,18 @@ class BlockVector {
         check(chebfd_block_create(a.get(), width, &h));
         h_.reset(h);
     }
+    // a zero-filled block with the rows (partition, halos) of `like`, `width` columns
+    BlockVector(const BlockVector& like, Index width) {
+        chebfd_block* h = nullptr;
+        check(chebfd_block_create_like(like.get(), width, &h));
+        h_.reset(h);
+    }
+    BlockVector() = default;  // empty (as the reference's default-constructed BlockVector)
     explicit BlockVector(chebfd_block* h) : h_(h) {}
-    Index dim() const { return info(1); }
-    Index width() const { return info(2); }
+    BlockVector(BlockVector&&) noexcept = default;
+    BlockVector& operator=(BlockVector&&) noexcept = default;
+    Index dim() const { return h_ ? info(1) : 0; }
+    Index width() const { return h_ ? info(2) : 0; }
     void upload(const std::vector<S>& host) {
         if (static_cast<Index>(host.size()) != dim() * width())
             throw std::invalid_argument("BlockVector::upload: size mismatch");
@@ -276,11 +285,11 @@ std::vector<double> column_norms(const BlockVector<S>& X) {
     return n;
 }
 
+// block_mult_small (kernels.hpp:216-232): Y = X B, B a small n_b x m row-major matrix
 template <class S>
-BlockVector<S> block_mult_small(const SparseMatrix<S>& A, const BlockVector<S>& X,
-                                const DenseMatrix<S>& B) {
+BlockVector<S> block_mult_small(const BlockVector<S>& X, const DenseMatrix<S>& B) {
     if (X.width() != B.rows) throw std::invalid_argument("block_mult_small: shape mismatch");
-    BlockVector<S> Y(A, B.cols);
+    BlockVector<S> Y(X, B.cols);
     check(chebfd_block_mult_small(X.get(), B.a.data(), B.cols, Y.get()));
     return Y;
 }
@@ -350,6 +359,10 @@ std::optional<MomentTable> apply_filter(const SparseMatrix<S>& A, BlockVector<S>
 template <class S>
 std::optional<MomentTable> apply_filter_host(const SparseMatrix<S>& A, std::vector<S>& x, Index width,
                                              const FilterPolynomial& p, bool want_moments = false) {
+    if (width < 1 || static_cast<Index>(x.size()) != A.info().local_rows * width)
+        throw std::invalid_argument("apply_filter_host: x must hold local_rows x width entries");
+    if (p.degree >= 2 && static_cast<Index>(p.combined.size()) < p.degree + 1)
+        throw std::invalid_argument("apply_filter: coefficient array shorter than degree+1");
     std::optional<MomentTable> mt;
     if (want_moments)
         mt = MomentTable{p.degree, width, std::vector<double>(static_cast<size_t>((p.degree + 1) * width))};
@@ -378,18 +391,110 @@ class FilterPipe {
     chebfd_filter_pipe* h_ = nullptr;
 };
 
-// ---- solver / spectral (solver.hpp, spectral.hpp) ------------------------------------------------
+// ---- spectral (spectral.hpp) ----------------------------------------------------------------
 inline Interval lanczos_bounds_of(chebfd_matrix* a, int iters, std::uint64_t seed) {
     Interval b;
     check(chebfd_lanczos_bounds(a, iters, seed, &b.lo, &b.hi));
     return b;
 }
 
+// lanczos_bounds (spectral.cpp:96-154)
 template <class S>
 Interval lanczos_bounds(const SparseMatrix<S>& A, int iters, std::uint64_t seed = 1) {
     return lanczos_bounds_of(A.get(), iters, seed);
 }
 
+// ChebSeriesDensity (spectral.hpp:14-33): raw moments on [a, b], Jackson-damped
+// reconstruction (density) and closed-form integral (count)
+class ChebSeriesDensity {
+  public:
+    ChebSeriesDensity() = default;
+    ChebSeriesDensity(std::vector<double> moments, Interval bounds)
+        : moments_(std::move(moments)), bounds_(bounds) {
+        if (moments_.empty()) throw std::invalid_argument("ChebSeriesDensity: no moments");
+        if (!(bounds.lo < bounds.hi)) throw std::invalid_argument("ChebSeriesDensity: bad bounds");
+    }
+    const std::vector<double>& moments() const { return moments_; }
+    Interval bounds() const { return bounds_; }
+    int order() const { return static_cast<int>(moments_.size()) - 1; }
+    double density(double lambda) const {
+        double out = 0.0;
+        check(chebfd_dos_density(moments_.data(), order(), bounds_.lo, bounds_.hi, lambda, &out));
+        return out;
+    }
+    double count(double lo, double hi) const {
+        double out = 0.0;
+        check(chebfd_dos_count(moments_.data(), order(), bounds_.lo, bounds_.hi, lo, hi, &out));
+        return out;
+    }
+    double total() const { return moments_.empty() ? 0.0 : moments_[0]; }
+
+  private:
+    std::vector<double> moments_;
+    Interval bounds_;
+};
+
+// DosEstimate (spectral.hpp:36-56)
+class DosEstimate {
+  public:
+    DosEstimate() = default;
+    DosEstimate(std::vector<double> moments, Interval bounds, int num_samples, Index dim)
+        : series_(std::move(moments), bounds), num_samples_(num_samples), dim_(dim) {}
+    double density(double lambda) const { return series_.density(lambda); }
+    double count(double lo, double hi) const { return series_.count(lo, hi); }
+    Interval bounds() const { return series_.bounds(); }
+    const std::vector<double>& moments() const { return series_.moments(); }
+    int num_samples() const { return num_samples_; }
+    Index matrix_dim() const { return dim_; }
+
+  private:
+    ChebSeriesDensity series_;
+    int num_samples_ = 0;
+    Index dim_ = 0;
+};
+
+// WeightDensity (spectral.hpp:57-72): integrates to N_S over the full interval
+class WeightDensity {
+  public:
+    WeightDensity() = default;
+    WeightDensity(std::vector<double> moments, Interval bounds) : series_(std::move(moments), bounds) {}
+    double density(double lambda) const { return series_.density(lambda); }
+    double count(double lo, double hi) const { return series_.count(lo, hi); }
+    double integral() const { return series_.total(); }
+    Interval bounds() const { return series_.bounds(); }
+    const std::vector<double>& moments() const { return series_.moments(); }
+
+  private:
+    ChebSeriesDensity series_;
+};
+
+// weight_density (spectral.cpp:81-88)
+inline WeightDensity weight_density(const MomentTable& moments, Interval bounds) {
+    if (moments.width == 0 || moments.m.empty())
+        throw std::invalid_argument("weight_density: empty moment table");
+    std::vector<double> mu(static_cast<size_t>(moments.degree) + 1);
+    check(chebfd_weight_density(moments.m.data(), static_cast<int>(moments.degree), moments.width,
+                                mu.data()));
+    return WeightDensity(std::move(mu), bounds);
+}
+
+// kpm_dos (spectral.cpp:156-205): stochastic-trace KPM DOS on the device
+template <class S>
+DosEstimate kpm_dos(const SparseMatrix<S>& A, Interval bounds, int order, int num_samples,
+                    std::uint64_t seed = 1) {
+    std::vector<double> mu(static_cast<size_t>(order < 0 ? 0 : order) + 1);
+    check(chebfd_kpm_dos(A.get(), bounds.lo, bounds.hi, order, num_samples, seed, mu.data()));
+    return DosEstimate(std::move(mu), bounds, num_samples, A.dim());
+}
+
+// estimate_count (spectral.cpp:90-94)
+inline double estimate_count(const DosEstimate& dos, Interval interval) {
+    if (!dos.bounds().contains(interval))
+        throw std::invalid_argument("estimate_count: interval outside DOS bounds");
+    return dos.count(interval.lo, interval.hi);
+}
+
+// ---- solver (solver.hpp) ------------------------------------------------------------------------
 struct SolverOptions {
     Interval target;
     double epsilon = 1e-10;
@@ -405,21 +510,84 @@ struct SolverOptions {
     bool collect_weight_density = true;
 };
 
+// RitzSet (solver.hpp:27-33)
+template <class S>
+struct RitzSet {
+    std::vector<double> values;          // ascending
+    BlockVector<S> vectors;              // orthonormal columns (device)
+    std::vector<double> residual_norms;  // ||A v - lambda v||
+    std::vector<bool> accepted;
+};
+
+struct IterationStat {
+    int iteration = 0;
+    double min_residual = 0.0;
+    double max_residual = 0.0;
+    int accepted_count = 0;
+    double cumulative_spmvms = 0.0;
+};
+
+// ConvergenceReport (solver.hpp:43-60)
+template <class S>
 struct ConvergenceReport {
     bool converged = false;
     int iterations = 0;
     double total_spmvms = 0.0;
-    int n_search = 0, degree = 0;
-    double sigma = 0.0, eta = 0.0;
+    int n_search = 0;
+    int degree = 0;
+    double sigma = 0.0;
+    double eta = 0.0;
     Interval bounds;
-    double matrix_norm_est = 0.0, n_target_estimate = 0.0;
-    std::vector<double> values, residual_norms;
-    std::vector<bool> accepted;
-    double weight_integral = 0.0, seconds = 0.0;
+    double matrix_norm_est = 0.0;
+    double n_target_estimate = 0.0;
+    RitzSet<S> ritz;
+    std::vector<IterationStat> history;
+    WeightDensity weight;
+    bool have_weight = false;
+    double seconds = 0.0;
+};
+
+// SvqbResult / svqb_orthonormalize (solver.hpp:64-71, solver.cpp:32-61)
+template <class S>
+struct SvqbResult {
+    BlockVector<S> q;
+    Index rank = 0;
 };
 
 template <class S>
-ConvergenceReport solve(const SparseMatrix<S>& A, const SolverOptions& o) {
+SvqbResult<S> svqb_orthonormalize(const BlockVector<S>& y, double drop_tol = 1e-14) {
+    BlockVector<S> q(y, y.width());
+    std::int64_t rank = 0;
+    check(chebfd_svqb(y.get(), drop_tol, q.get(), &rank));
+    SvqbResult<S> out;
+    out.rank = rank;
+    if (rank == y.width()) {
+        out.q = std::move(q);
+    } else {  // the reference returns exactly `rank` columns
+        BlockVector<S> qr(y, rank);
+        check(chebfd_block_copy_columns(qr.get(), 0, q.get(), 0, rank));
+        out.q = std::move(qr);
+    }
+    return out;
+}
+
+// rayleigh_ritz (solver.hpp:73-75, solver.cpp:63-91)
+template <class S>
+RitzSet<S> rayleigh_ritz(const SparseMatrix<S>& A, const BlockVector<S>& q) {
+    RitzSet<S> r;
+    r.vectors = BlockVector<S>(q, q.width());
+    r.values.resize(static_cast<size_t>(q.width()));
+    r.residual_norms.resize(static_cast<size_t>(q.width()));
+    check(chebfd_rayleigh_ritz(A.get(), q.get(), r.vectors.get(), r.values.data(),
+                               r.residual_norms.data()));
+    r.accepted.assign(static_cast<size_t>(q.width()), false);
+    return r;
+}
+
+// solve (solver.hpp:77-80, solver.cpp:93-214): the host loop of the reference with
+// every block operation on the device
+template <class S>
+ConvergenceReport<S> solve(const SparseMatrix<S>& A, const SolverOptions& o) {
     chebfd_solver_options c{};
     chebfd_solver_options_default(&c);
     c.target_lo = o.target.lo;
@@ -438,10 +606,15 @@ ConvergenceReport solve(const SparseMatrix<S>& A, const SolverOptions& o) {
     c.collect_weight_density = o.collect_weight_density ? 1 : 0;
     chebfd_solve_report r{};
     const int cap = 4096 + 2 * o.n_search;
-    std::vector<double> vals(cap), res(cap);
+    std::vector<double> vals(cap), res(cap), hist(static_cast<size_t>(5 * std::max(o.max_iters, 1)));
     std::vector<int> acc(cap);
-    check(chebfd_solve(A.get(), &c, &r, cap, vals.data(), res.data(), acc.data(), nullptr, nullptr));
-    ConvergenceReport out;
+    const int wcap = 1 << 20;
+    std::vector<double> wmu(wcap);
+    int wlen = 0;
+    chebfd_block* vh = nullptr;
+    check(chebfd_solve_ex(A.get(), &c, &r, cap, vals.data(), res.data(), acc.data(), hist.data(),
+                          &vh, wcap, wmu.data(), &wlen));
+    ConvergenceReport<S> out;
     out.converged = r.converged != 0;
     out.iterations = r.iterations;
     out.total_spmvms = r.total_spmvms;
@@ -452,10 +625,18 @@ ConvergenceReport solve(const SparseMatrix<S>& A, const SolverOptions& o) {
     out.bounds = {r.bounds_lo, r.bounds_hi};
     out.matrix_norm_est = r.matrix_norm_est;
     out.n_target_estimate = r.n_target_estimate;
-    out.values.assign(vals.begin(), vals.begin() + r.n_values);
-    out.residual_norms.assign(res.begin(), res.begin() + r.n_values);
-    for (int k = 0; k < r.n_values; ++k) out.accepted.push_back(acc[k] != 0);
-    out.weight_integral = r.weight_integral;
+    out.ritz.values.assign(vals.begin(), vals.begin() + r.n_values);
+    out.ritz.residual_norms.assign(res.begin(), res.begin() + r.n_values);
+    for (int k = 0; k < r.n_values; ++k) out.ritz.accepted.push_back(acc[k] != 0);
+    if (vh) out.ritz.vectors = BlockVector<S>(vh);
+    for (int i = 0; i < r.iterations; ++i) {
+        const double* h = hist.data() + 5 * i;
+        out.history.push_back({static_cast<int>(h[0]), h[1], h[2], static_cast<int>(h[3]), h[4]});
+    }
+    if (wlen > 0) {
+        out.weight = WeightDensity(std::vector<double>(wmu.begin(), wmu.begin() + wlen), out.bounds);
+        out.have_weight = true;
+    }
     out.seconds = r.seconds;
     return out;
 }

@@ -16,8 +16,9 @@ from .api import (  # noqa: F401
     window_coeffs, DesignResult, choose_parameters, damping_factor, invert_search_margin,
     optimize_degree, quality, host_randomize, read_matrix_market, write_matrix_market,
     save_block, load_block, BenchPoint, BenchReport, bandwidth_probe, bandwidth_probe_min_bytes,
-    bench_filter, FilterPipe, host_array,
+    bench_filter, FilterPipe, host_array, experimental_build,
+    filter_schedule_bytes, WeightDensity, weight_density,
 )
 from ._lib import LIB_PATH, load  # noqa: F401
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

@@ -72,6 +72,12 @@ def _check(rc):
         raise _EXC.get(rc, ChebfdError)(msg)
 
 
+def experimental_build() -> bool:
+    """True when the library was built with the opt-in slower kernel variants
+    (make EXPERIMENTAL=1): the pair kernel and kernel variant 2."""
+    return bool(_lib().chebfd_build_features() & 1)
+
+
 def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -161,7 +167,8 @@ class Context:
         ("direct" | "doubling": how filter / KPM moments are formed)."""
         code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5, "pair": 6,
                 "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
-                "pair_slab": 11, "moments": 12, "pdl": 14, "delayed_x": 15}[name]
+                "pair_slab": 11, "moments": 12, "pdl": 14, "delayed_x": 15,
+                "band_bytes": 16, "async_start": 17, "tiles_per_cta": 18}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):
@@ -595,7 +602,12 @@ def apply_filter_host(A: SparseMatrix, x: np.ndarray, p: FilterPolynomial,
     """End-to-end filter of a HOST block (in place): H2D, filter, D2H."""
     if x.dtype != A.dtype or not x.flags.c_contiguous:
         raise InvalidArgument("apply_filter_host: x must be C-contiguous of the matrix dtype")
+    if x.ndim != 2 or x.shape[0] != A.local_rows or x.shape[1] < 1:
+        raise InvalidArgument("apply_filter_host: x must be (local rows x width) "
+                              f"= ({A.local_rows}, n_b), got {x.shape}")
     comb = np.ascontiguousarray(p.combined, dtype=np.float64)
+    if p.degree >= 2 and len(comb) < p.degree + 1:
+        raise InvalidArgument("apply_filter: coefficient array shorter than degree+1")
     mom = np.empty((p.degree + 1, x.shape[1])) if want_moments else None
     _check(_lib().chebfd_apply_filter_host(A._h, _ptr(x), x.shape[1], _ptr(comb), p.degree,
                                            p.alpha, p.beta, _ptr(mom)))
@@ -710,6 +722,42 @@ class DosEstimate:
                                        lo, hi, C.byref(out)))
         return out.value
 
+    def density(self, lam) -> float:
+        """ChebSeriesDensity::density (spectral.cpp:31-44)."""
+        mu = np.ascontiguousarray(self.moments, dtype=np.float64)
+        out = C.c_double()
+        _check(_lib().chebfd_dos_density(_ptr(mu), len(mu) - 1, self.bounds.lo, self.bounds.hi,
+                                         float(lam), C.byref(out)))
+        return out.value
+
+
+@dataclass
+class WeightDensity:
+    """Search-space weight density w(lambda) (spectral.hpp:57-72): the summed filter
+    moments as a Jackson-damped Chebyshev series; integrates to N_S."""
+    moments: np.ndarray
+    bounds: Interval
+
+    def _series(self):
+        return DosEstimate(self.moments, self.bounds)
+
+    def density(self, lam) -> float:
+        return self._series().density(lam)
+
+    def count(self, lo, hi) -> float:
+        return self._series().count(lo, hi)
+
+    def integral(self) -> float:
+        return float(self.moments[0]) if len(self.moments) else 0.0
+
+
+def weight_density(moments: "MomentTable", bounds) -> WeightDensity:
+    """spectral.cpp:81-88: mu[n] = sum_k m(n, k)."""
+    m = np.ascontiguousarray(moments.m, dtype=np.float64)
+    mu = np.empty(max(int(moments.degree), 0) + 1)
+    _check(_lib().chebfd_weight_density(_ptr(m), int(moments.degree), int(moments.width), _ptr(mu)))
+    return WeightDensity(mu, _iv(bounds))
+
 
 def kpm_dos(A: SparseMatrix, bounds, order: int, num_samples: int, seed: int = 1) -> DosEstimate:
     """spectral.cpp:156-205"""
@@ -763,6 +811,7 @@ class ConvergenceReport:
     have_weight: bool
     seconds: float
     timings: dict = field(default_factory=dict)  # wall seconds per solve phase
+    weight: Optional["WeightDensity"] = None     # ConvergenceReport::weight (solver.cpp:158-162)
 
 
 def solve(A: SparseMatrix, opts: SolverOptions) -> ConvergenceReport:
@@ -791,8 +840,14 @@ def solve(A: SparseMatrix, opts: SolverOptions) -> ConvergenceReport:
     acc = np.zeros(cap, dtype=np.int32)
     hist = np.zeros((opts.max_iters, 5))
     vh = C.c_void_p()
-    _check(_lib().chebfd_solve(A._h, C.byref(o), C.byref(rep), cap, _ptr(vals), _ptr(res),
-                               _ptr(acc), _ptr(hist), C.byref(vh)))
+    wcap = 1 << 20
+    wmu = np.zeros(wcap)
+    wlen = C.c_int()
+    _check(_lib().chebfd_solve_ex(A._h, C.byref(o), C.byref(rep), cap, _ptr(vals), _ptr(res),
+                                  _ptr(acc), _ptr(hist), C.byref(vh), wcap, _ptr(wmu),
+                                  C.byref(wlen)))
+    weight = (WeightDensity(wmu[:wlen.value].copy(), Interval(rep.bounds_lo, rep.bounds_hi))
+              if wlen.value > 0 else None)
     n = rep.n_values
     V = BlockVector(A, _handle=vh) if vh.value else None
     ritz = RitzSet(vals[:n].copy(), V, res[:n].copy(), acc[:n].astype(bool))
@@ -802,7 +857,8 @@ def solve(A: SparseMatrix, opts: SolverOptions) -> ConvergenceReport:
                              hist[:rep.iterations].copy(), rep.weight_integral,
                              bool(opts.collect_weight_density), rep.seconds,
                              {k: getattr(rep, "t_" + k) for k in
-                              ("bounds", "dos", "design", "filter", "ortho", "rr", "start")})
+                              ("bounds", "dos", "design", "filter", "ortho", "rr", "start")},
+                             weight)
 
 
 # ----------------------------------------------------- bench conventions --
@@ -814,6 +870,26 @@ def per_row_flops(n_nzr, f_a, f_m):
 def per_row_bytes(n_nzr, s_d, s_i, n_b):
     """bench.cpp:32-34"""
     return n_nzr / n_b * (s_d + s_i) + 5.0 * s_d
+
+
+def filter_schedule_bytes(dim, nnz, n_b, cplx, degree, group=3):
+    """Minimal DRAM bytes of one apply_filter as this library schedules it (no moments):
+    the matrix (S_d + 4 bytes per entry) once per step plus the block streams each step
+    kind moves -- start-up spmmvm (X gathered, U written: 2 streams), start-up step 2 (U
+    gathered, X read, W and X written: 4), then groups of `group` steps (CHEBFD_OPT_DELAYED_X):
+    V_n-only steps (U gathered, W read and written: 3) and the group's last step, which
+    also reads and writes X (5).  The reference's model (bench.cpp:32-34) charges 5
+    streams to every step; this is the byte count the kernels can at best move."""
+    s_d = 16 if cplx else 8
+    mat = nnz * (s_d + 4)
+    blk = dim * n_b * s_d
+    total = (mat + 2 * blk) + (mat + 4 * blk)
+    n = 3
+    while n <= degree:
+        g = min(max(group, 1), degree - n + 1)
+        total += (g - 1) * (mat + 3 * blk) + (mat + 5 * blk)
+        n += g
+    return total
 
 
 def intensity_model(n_nzr, s_d, s_i, f_a, f_m, n_b):

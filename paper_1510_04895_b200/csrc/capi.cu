@@ -496,6 +496,10 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
     const int64_t nnz_g = allreduce_count(c, static_cast<int64_t>(csr.cols.size()));
     auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g);
     m->hermitian = true;  // both models add every hopping with its conjugate (models.cpp:80-178)
+    if (ti) {  // row = 4 (x + Lx (y + Ly z)) + orbital (models.hpp:15-19)
+        m->plane_rows = 4 * s.lx * s.ly;
+        m->line_rows = 4 * s.lx;
+    }
     return m;
 }
 
@@ -753,7 +757,9 @@ using namespace cfd;
 extern "C" {
 
 const char* chebfd_last_error(void) { return g_last_error.c_str(); }
-const char* chebfd_version(void) { return "chebfd_b200 0.1 (sm_100a)"; }
+const char* chebfd_version(void) { return "chebfd_b200 0.2 (sm_100a)"; }
+
+int chebfd_build_features(void) { return CFD_EXPERIMENTAL ? CHEBFD_FEATURE_EXPERIMENTAL : 0; }
 
 int chebfd_nccl_unique_id(unsigned char id[128]) {
     return guard([&] {
@@ -854,18 +860,30 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->use_graphs = value != 0;
         else if (option == CHEBFD_OPT_OVERLAP)
             c->overlap = value != 0;
-        else if (option == CHEBFD_OPT_KERNEL)
+        else if (option == CHEBFD_OPT_KERNEL) {
+            if (value == 2 && !CFD_EXPERIMENTAL)
+                fail(CHEBFD_ERR_UNSUPPORTED, "kernel variant 2 (staged gathers) needs an EXPERIMENTAL=1 build");
             c->kernel_variant = static_cast<int>(value);
+        }
         else if (option == CHEBFD_OPT_SLAB_UNITS)
             c->slab_units = static_cast<int>(value);
-        else if (option == CHEBFD_OPT_PAIR)
+        else if (option == CHEBFD_OPT_PAIR) {
+            if (value != 0 && !CFD_EXPERIMENTAL)
+                fail(CHEBFD_ERR_UNSUPPORTED, "the pair kernel needs an EXPERIMENTAL=1 build");
             c->pair_mode = static_cast<int>(value);
+        }
         else if (option == CHEBFD_OPT_MOMENTS)
             c->moments_mode = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PDL)
             c->pdl = static_cast<int>(value);
         else if (option == CHEBFD_OPT_DELAYED_X)
             c->delayed_x = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_BAND_BYTES)
+            c->band_bytes = value;
+        else if (option == CHEBFD_OPT_ASYNC_START)
+            c->async_start_entries = value;
+        else if (option == CHEBFD_OPT_TILES_PER_CTA)
+            c->tiles_per_cta = static_cast<int>(std::max<int64_t>(value, 0));
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
             c->pair_tile_rows = static_cast<int>(value);
         else if (option == CHEBFD_OPT_PAIR_THREADS)
@@ -1035,6 +1053,19 @@ int chebfd_block_create_dim(chebfd_ctx* ctx, int kind, int64_t dim, int64_t widt
         Context& c = *reinterpret_cast<Context*>(ctx);
         require(kind == CHEBFD_REAL64 || kind == CHEBFD_COMPLEX128, "bad scalar kind");
         auto b = make_block(c, nullptr, kind, dim, width);
+        *out = reinterpret_cast<chebfd_block*>(b.release());
+    });
+}
+
+int chebfd_block_create_like(const chebfd_block* like, int64_t width, chebfd_block** out) {
+    return guard([&] {
+        require(like != nullptr && out != nullptr, "block_create_like: null argument");
+        const Block& l = *reinterpret_cast<const Block*>(like);
+        std::unique_ptr<Block> b;
+        if (l.shape_of)
+            b = make_block(*l.ctx, l.shape_of, l.kind, l.rows, width);
+        else
+            b = make_block(*l.ctx, nullptr, l.kind, l.rows, width);
         *out = reinterpret_cast<chebfd_block*>(b.release());
     });
 }

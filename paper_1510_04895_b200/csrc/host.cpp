@@ -299,6 +299,27 @@ double dos_count(const double* mu, int order, double blo, double bhi, double lo,
     return acc / kPi;
 }
 
+// ChebSeriesDensity::density (spectral.cpp:31-44): Jackson-damped reconstruction at lambda
+double dos_density(const double* mu, int order, double blo, double bhi, double lambda) {
+    if (order < 0) fail(CHEBFD_ERR_INVALID_ARGUMENT, "ChebSeriesDensity: no moments");
+    if (!(blo < bhi)) fail(CHEBFD_ERR_INVALID_ARGUMENT, "ChebSeriesDensity: bad bounds");
+    const double alpha = 2.0 / (bhi - blo);
+    const double beta = (blo + bhi) / (blo - bhi);
+    const auto g = kernel_coeffs(CHEBFD_KERNEL_JACKSON, 0, std::max(order, 1));
+    double x = alpha * lambda + beta;
+    x = std::clamp(x, -1.0 + 1e-12, 1.0 - 1e-12);
+    double acc = g[0] * mu[0];
+    double tm2 = 1.0, tm1 = x;
+    if (order >= 1) acc += 2.0 * (g[1] * mu[1]) * x;
+    for (int n = 2; n <= order; ++n) {
+        const double tn = 2.0 * x * tm1 - tm2;
+        acc += 2.0 * (g[n] * mu[n]) * tn;
+        tm2 = tm1;
+        tm1 = tn;
+    }
+    return alpha * acc / (kPi * std::sqrt(1.0 - x * x));
+}
+
 void plane_partition(int64_t dim, int64_t plane, int rank, int nranks, int64_t* r0, int64_t* r1) {
     const int64_t planes = plane > 0 ? dim / plane : dim;
     const int64_t unit = plane > 0 ? plane : 1;

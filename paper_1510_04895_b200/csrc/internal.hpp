@@ -13,6 +13,13 @@
 
 #include "../../include/chebfd_b200.h"
 
+// Opt-in kernel variants that measured slower than the default path (the two-step
+// wavefront pair kernel, pair.cu, and the staged-gather step kernel, kernel variant 2;
+// DESIGN.md §5): compiled only with -DCFD_EXPERIMENTAL=1 (make EXPERIMENTAL=1).
+#ifndef CFD_EXPERIMENTAL
+#define CFD_EXPERIMENTAL 0
+#endif
+
 struct cublasContext;
 struct cusolverDnContext;
 typedef struct ncclComm* ncclComm_t;
@@ -118,6 +125,9 @@ struct Matrix {
     bool hermitian = false; // bitwise A = A^H (lattice models; checked for from_csr input):
                             // enables moment doubling
     int64_t band = 0;       // max |extended column - extended row| over all entries
+    // lattice structure of model operators (0: unknown): rows per z-plane and per lattice
+    // line (TI: 4 Lx Ly and 4 Lx); the step kernels' band tile order uses it
+    int64_t plane_rows = 0, line_rows = 0;
     DeviceBuffer pair_sync; // pair kernel: item / exit tickets + per-1024-row group counters (zeroed)
 };
 
@@ -193,11 +203,20 @@ struct Context {
     // apply_filter: X read and written every delayed_x-th step (kStepRecur steps, then
     // kStepFusedX2 / X3 adding their terms); 0 or 1: every step
     int delayed_x = 3;
+    // band tile order of lattice operators: a band slice of the gathered operand is at
+    // most this many bytes (0: row order everywhere); CHEBFD_OPT_BAND_BYTES
+    int64_t band_bytes = int64_t(16) << 20;
+    // solve with N_S given: blocks of at least this many entries get their start block
+    // generated on a helper thread during bounds + KPM (0: never); CHEBFD_OPT_ASYNC_START
+    int64_t async_start_entries = int64_t(1) << 26;
     int pair_mode = 0, pair_tile_rows = 0, pair_threads = 0, pair_extra = -1, pair_hints = 1,
         pair_slab = 0;
     // reduction scratch shared by all kernels on `stream` (stream-ordered reuse)
     DeviceBuffer partials;   // per-block partial sums
     DeviceBuffer counter;    // last-block-done ticket (uint32), self-resetting
+    // step launches without dots: non-persistent grids of this many consecutive row tiles
+    // per CTA (0: persistent CTA-strided grids everywhere); CHEBFD_OPT_TILES_PER_CTA
+    int tiles_per_cta = 2;
     DeviceBuffer dscratch;   // small device results (dots, Gram, moments)
     DeviceBuffer workspace;  // cuSOLVER / misc
     DeviceBuffer devinfo;
@@ -253,6 +272,11 @@ struct StepArgs {
     bool pdl_ok;             // may launch as a programmatic dependent of the previous kernel
 };
 void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st);
+// per-layout step dispatch (step_c.cu / step_r2.cu / step_r1.cu): units = 16- or 8-byte
+// units per row
+void launch_step_c(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
+void launch_step_r2(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
+void launch_step_r1(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
 // column-slab launches launch_step will use for s (an upper bound: >= the real count)
 int step_slab_count(const Context& ctx, const StepArgs& s);
 // Steps coeff_index and coeff_index+1 of apply_filter's fused loop in one
@@ -317,6 +341,7 @@ class NormalStream {
 std::vector<double> window_coeffs(double tlo, double thi, double blo, double bhi, int degree);
 std::vector<double> kernel_coeffs(int kind, int mu, int degree);
 double dos_count(const double* mu, int order, double blo, double bhi, double lo, double hi);
+double dos_density(const double* mu, int order, double blo, double bhi, double lambda);
 struct HostCsr;
 // Halos of rows [r0, r1) derived from the global columns they read (ring
 // distance decides lower vs upper neighbour); starts[q] = first row of rank q.

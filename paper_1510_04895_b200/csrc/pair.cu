@@ -46,6 +46,8 @@
 
 namespace cfd {
 
+#if CFD_EXPERIMENTAL  // opt-in variant, measured slower; not in the default build
+
 namespace {
 
 constexpr int kGroupChunksLog2 = 5;  // 32 chunks (1024 rows) per completion group
@@ -517,5 +519,9 @@ bool launch_step_pair(Context& ctx, const StepArgs& s, cudaStream_t st) {
                                           static_cast<int>(width / 2));
     return pair_width<false, double>(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
 }
+
+#else
+bool launch_step_pair(Context&, const StepArgs&, cudaStream_t) { return false; }
+#endif  // CFD_EXPERIMENTAL
 
 }  // namespace cfd

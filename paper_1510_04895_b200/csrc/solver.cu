@@ -373,10 +373,37 @@ void chebfd_solver_options_default(chebfd_solver_options* o) {
     o->collect_weight_density = 1;
 }
 
+int chebfd_dos_density(const double* mu, int order, double blo, double bhi, double lambda,
+                       double* out) {
+    return guard([&] { *out = dos_density(mu, order, blo, bhi, lambda); });
+}
+
+int chebfd_weight_density(const double* moments, int degree, int64_t width, double* mu) {
+    return guard([&] {
+        // weight_density (spectral.cpp:81-88): mu[n] = sum_k m(n, k), k in column order
+        if (width <= 0 || degree < 0 || moments == nullptr)
+            fail(CHEBFD_ERR_INVALID_ARGUMENT, "weight_density: empty moment table");
+        for (int n = 0; n <= degree; ++n) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < width; ++k) acc += moments[static_cast<int64_t>(n) * width + k];
+            mu[n] = acc;
+        }
+    });
+}
+
 int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_report* rep,
                  int cap, double* values, double* residual_norms, int* accepted, double* history,
                  chebfd_block** vectors) {
+    return chebfd_solve_ex(a, o, rep, cap, values, residual_norms, accepted, history, vectors, 0,
+                           nullptr, nullptr);
+}
+
+int chebfd_solve_ex(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_report* rep,
+                    int cap, double* values, double* residual_norms, int* accepted,
+                    double* history, chebfd_block** vectors, int weight_cap,
+                    double* weight_moments, int* weight_len) {
     return guard([&] {
+        if (weight_len) *weight_len = 0;
         Matrix& A = *reinterpret_cast<Matrix*>(a);
         Context& c = *A.ctx;
         const auto t0 = std::chrono::steady_clock::now();
@@ -396,7 +423,8 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
         std::unique_ptr<AsyncRandomize> x_job;
         // (only for blocks whose generation takes longer than the helper's set-up: pinned
         // buffers and a stream cost ~50 ms, a C1 block takes 6 ms synchronously)
-        if (o->n_search > 0 && A.part.local * o->n_search >= (int64_t{1} << 26)) {
+        if (o->n_search > 0 && c.async_start_entries > 0 &&
+            A.part.local * o->n_search >= c.async_start_entries) {
             x_early = make_block(c, &A, A.kind, A.part.local, o->n_search, false);
             ctx_sync(c);  // the (cached) storage and its halo clear are settled on c.stream
             x_job = std::make_unique<AsyncRandomize>(c, *x_early, o->seed + 2);
@@ -484,9 +512,21 @@ int chebfd_solve(chebfd_matrix* a, const chebfd_solver_options* o, chebfd_solve_
             rep->t_filter += secs(tp);
             tp = clk::now();
             if (o->collect_weight_density) {
-                double w0 = 0.0;  // weight_density mu[0] = sum_k m(0,k) (spectral.cpp:81-88)
+                // rep.weight = weight_density(moments, bounds) of this iteration's filter
+                // (solver.cpp:158-162, spectral.cpp:81-88): mu[n] = sum_k m(n, k)
+                double w0 = 0.0;
                 for (int64_t k = 0; k < x->width; ++k) w0 += mom[k];
                 rep->weight_integral = w0;
+                if (weight_moments) {
+                    if (weight_cap < np + 1)
+                        fail(CHEBFD_ERR_INVALID_ARGUMENT, "solve: weight capacity too small");
+                    for (int n = 0; n <= np; ++n) {
+                        double acc = 0.0;
+                        for (int64_t k = 0; k < x->width; ++k) acc += mom[static_cast<size_t>(n) * x->width + k];
+                        weight_moments[n] = acc;
+                    }
+                    if (weight_len) *weight_len = np + 1;
+                }
             }
             SvqbOut ortho = svqb(c, &A, *x, 1e-14);
             for (int repair = 0; ortho.rank < ns && repair < 5; ++repair) {

@@ -306,7 +306,38 @@ struct StepParams {
     int final_launch;
     unsigned* counter;
     int tr;  // minimum rows per tile of the TMA kernels (32 or 64)
+    // band (2.5D) tile order of the TMA kernel for lattice operators: the
+    // launch's rows are whole lattice planes of band_plane_chunks chunks; tiles enumerate
+    // (band, plane, tile in the band's slice of the plane), so the z -+ 1 planes a tile
+    // gathers were touched one slice (not one plane) earlier.  band_tps = 0: row order.
+    // Divisions by the invariant tiles-per-band / tiles-per-slice use host-computed
+    // reciprocals M = ceil(2^64 / d) (exact for 32-bit numerators), so the mapping costs
+    // a few multiplies and no registers in the row loop.
+    unsigned band_tps;          // tiles per band slice (0: row order)
+    unsigned band_per_band;     // tiles per band (planes x band_tps)
+    uint64_t band_m_tps, band_m_per_band;
+    int64_t band_plane_chunks;  // 32-row chunks per plane
+    int64_t band_slice_chunks;  // 32-row chunks per band slice
+    int64_t tile_a;             // tiles per CTA of a non-persistent (ORDER 1) launch
 };
+
+// n / d for 32-bit n with the host reciprocal m = ceil(2^64 / d) (d >= 2), or n (d == 1)
+__device__ __forceinline__ unsigned div_by(unsigned n, unsigned d, uint64_t m) {
+    return d == 1u ? n : static_cast<unsigned>(__umul64hi(static_cast<uint64_t>(n), m));
+}
+
+// first chunk of tile `tile` of a launch starting at chunk cbeg (NCH chunks per tile)
+__device__ __forceinline__ int64_t tile_first_chunk(const StepParams& p, int64_t tile, int64_t cbeg,
+                                                    int NCH) {
+    if (p.band_tps == 0u) return cbeg + tile * NCH;
+    const unsigned tl = static_cast<unsigned>(tile);
+    const unsigned b = div_by(tl, p.band_per_band, p.band_m_per_band);
+    const unsigned rem = tl - b * p.band_per_band;
+    const unsigned z = div_by(rem, p.band_tps, p.band_m_tps);
+    const unsigned j = rem - z * p.band_tps;
+    return cbeg + static_cast<int64_t>(z) * p.band_plane_chunks +
+           static_cast<int64_t>(b) * p.band_slice_chunks + static_cast<int64_t>(j) * NCH;
+}
 
 // Sum_j (a_rj * scale) * in[c_rj] over one row, in the row's stored order.
 // MAXW > 0: all column indices of the row are loaded first, then every

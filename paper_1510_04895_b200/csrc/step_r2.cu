@@ -1,0 +1,9 @@
+// Step-kernel instantiations for one scalar layout (split from kernels.cu so the
+// three layouts compile in parallel).
+#include "step_kernels.cuh"
+
+namespace cfd {
+void launch_step_r2(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
+    dispatch_kind<false, double2>(ctx, s, st, units, pitch);
+}
+}  // namespace cfd

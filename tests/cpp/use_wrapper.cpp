@@ -114,6 +114,67 @@ int main(int argc, char** argv) {
     double worst = 0.0;
     for (size_t i = 0; i < md->m.size(); ++i) worst = std::max(worst, std::abs(md->m[i] - m->m[i]));
     EXPECT(worst <= 1e-12 * std::abs(m->m[0]));
+    // block_mult_small(X, B) (kernels.hpp:216-232): X times the identity is X
+    cb::DenseMatrix<cb::Complex> I(8, 3);
+    for (int k = 0; k < 3; ++k) I(k, k) = 1.0;
+    auto X3 = cb::block_mult_small(X, I);
+    EXPECT(X3.width() == 3 && X3.dim() == X.dim());
+    {
+        auto a = X.download(), b = X3.download();
+        bool same = true;
+        for (cb::Index i = 0; i < X.dim(); ++i)
+            for (int k = 0; k < 3; ++k) same = same && a[i * 8 + k] == b[i * 3 + k];
+        EXPECT(same);
+    }
+    // svqb_orthonormalize + rayleigh_ritz (solver.cpp:32-91): orthonormal Q, ascending
+    // values with residuals; a duplicated column drops the rank by one
+    auto sq = cb::svqb_orthonormalize(X);
+    EXPECT(sq.rank == 8 && sq.q.width() == 8);
+    auto Gq = cb::gram(sq.q, sq.q);
+    double off = 0.0;
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) off = std::max(off, std::abs(Gq(i, j) - (i == j ? 1.0 : 0.0)));
+    EXPECT(off < 1e-12);
+    cb::DenseMatrix<cb::Complex> dup(8, 8);
+    for (int k = 0; k < 8; ++k) dup(k, k) = 1.0;
+    dup(0, 7) = 1.0;
+    dup(7, 7) = 0.0;  // column 7 := column 0
+    auto Xd = cb::block_mult_small(X, dup);
+    auto sd = cb::svqb_orthonormalize(Xd);
+    EXPECT(sd.rank == 7 && sd.q.width() == 7);
+    auto rz = cb::rayleigh_ritz(A, sq.q);
+    EXPECT(rz.values.size() == 8 && rz.vectors.width() == 8 && rz.residual_norms.size() == 8);
+    EXPECT(std::is_sorted(rz.values.begin(), rz.values.end()));
+    // spectral.hpp: kpm_dos + estimate_count (interval outside the bounds throws)
+    auto bnd = cb::lanczos_bounds(A, 30, 1);
+    auto dos = cb::kpm_dos(A, bnd, 200, 8, 2);
+    EXPECT(dos.moments().size() == 201 && dos.num_samples() == 8 && dos.matrix_dim() == A.dim());
+    const double all = cb::estimate_count(dos, bnd);
+    EXPECT(std::abs(all - double(A.dim())) < 0.05 * double(A.dim()));
+    EXPECT(dos.density(0.5 * (bnd.lo + bnd.hi)) >= 0.0);
+    threw = false;
+    try {
+        cb::estimate_count(dos, {bnd.lo - 1.0, bnd.hi});
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    EXPECT(threw);
+    // weight_density of the filter moments integrates to the summed squared column norms
+    auto wd = cb::weight_density(*m, pf.bounds);
+    double m0 = 0.0;
+    for (int k = 0; k < 8; ++k) m0 += (*m)(0, k);
+    EXPECT(wd.integral() == m0 && wd.moments().size() == 41);
+    // solve (solver.cpp:93-214) on a tiny window: the report carries the Ritz set, the
+    // history and the weight density of the last filter (solver.cpp:158-162)
+    cb::SolverOptions so;
+    so.target = {-0.3, 0.3};
+    so.n_search = 16;
+    so.degree = 60;
+    auto rep = cb::solve(A, so);
+    EXPECT(rep.iterations >= 1 && static_cast<int>(rep.history.size()) == rep.iterations);
+    EXPECT(rep.have_weight && static_cast<int>(rep.weight.moments().size()) == rep.degree + 1);
+    EXPECT(std::abs(rep.weight.integral() - 16.0) < 1e-9);
+    EXPECT(rep.ritz.vectors.width() == static_cast<cb::Index>(rep.ritz.values.size()));
     std::printf("%s (device)\n", fails ? "FAILED" : "ok");
     return fails;
 }
