@@ -63,7 +63,10 @@ enum { CHEBFD_FEATURE_EXPERIMENTAL = 1 };
 int chebfd_build_features(void);
 
 /* ---- context --------------------------------------------------------------- */
-/* Single-GPU context on `device` (replaces the OpenMP runtime, parallel.hpp:18-54). */
+/* Single-GPU context on `device` (replaces the OpenMP runtime, parallel.hpp:18-54).
+ * One CUDA device per process (one process per GPU): creating a context on a second
+ * device while contexts on another exist fails with CHEBFD_ERR_UNSUPPORTED; several
+ * contexts on the same device are allowed. */
 int chebfd_ctx_create(int device, chebfd_ctx** out);
 /* Distributed context: this process is `rank` of `nranks`, one GPU each; the
  * 128-byte NCCL unique id comes from chebfd_nccl_unique_id() on rank 0 and is
@@ -337,6 +340,12 @@ typedef struct chebfd_filter_pipe chebfd_filter_pipe;
 int chebfd_filter_pipe_create(chebfd_matrix* a, int64_t width, chebfd_filter_pipe** out);
 int chebfd_filter_pipe_submit(chebfd_filter_pipe* p, const void* host_in, void* host_out,
                               const double* combined, int degree, double alpha, double beta);
+/* submit + the Rayleigh-Ritz Gram G = X^H X of the filtered block (gram(X, X),
+ * kernels.hpp:165-192; row-major width x width scalars, summed over ranks) copied to
+ * gram_host with the block; both valid after chebfd_filter_pipe_wait. */
+int chebfd_filter_pipe_submit_gram(chebfd_filter_pipe* p, const void* host_in, void* host_out,
+                                   const double* combined, int degree, double alpha,
+                                   double beta, void* gram_host);
 int chebfd_filter_pipe_wait(chebfd_filter_pipe* p);
 int chebfd_filter_pipe_destroy(chebfd_filter_pipe* p);
 

@@ -385,6 +385,11 @@ class FilterPipe {
     void submit(const S* in, S* out, const FilterPolynomial& p) {
         check(chebfd_filter_pipe_submit(h_, in, out, p.combined.data(), p.degree, p.alpha, p.beta));
     }
+    // ... and the Gram X^H X of the filtered block into gram (width x width, row-major)
+    void submit(const S* in, S* out, const FilterPolynomial& p, S* gram) {
+        check(chebfd_filter_pipe_submit_gram(h_, in, out, p.combined.data(), p.degree, p.alpha,
+                                             p.beta, gram));
+    }
     void wait() { check(chebfd_filter_pipe_wait(h_)); }
 
   private:

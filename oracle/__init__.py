@@ -346,6 +346,12 @@ class Ref:
         L.ref_block_mult_small.argtypes = [C.c_int, _i64, _i64, _vp, _vp, _i64, _vp]
         L.ref_apply_filter.argtypes = [_vp, _vp, _i64, _vp, C.c_int, _dbl, _dbl, _vp]
         L.ref_time_fused_steps.argtypes = [_vp, _i64, C.c_int, _dbl, _dbl, _dbl, _u64, _vp]
+        L.ref_fused_session_create.argtypes = [_vp, _i64, _vp]
+        L.ref_fused_session_run.argtypes = [_vp, C.c_int, _dbl, _dbl, _dbl, _vp]
+        L.ref_fused_session_apply.argtypes = [_vp, _vp, C.c_int, _dbl, _dbl, _vp]
+        L.ref_fused_session_gram.argtypes = [_vp, _vp]
+        L.ref_fused_session_free.argtypes = [_vp]
+        L.ref_fused_session_free.restype = None
         L.ref_svqb.argtypes = [C.c_int, _i64, _i64, _vp, _dbl, _vp, _vp]
         L.ref_rayleigh_ritz.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp]
         L.ref_lanczos_bounds.argtypes = [_vp, C.c_int, _u64, _vp, _vp]
@@ -481,6 +487,42 @@ class Ref:
         self._chk(self.lib.ref_time_fused_steps(m.h, width, steps, alpha, beta, coeff, seed,
                                                 C.byref(sec)))
         return sec.value
+
+    def fused_session(self, m, width):
+        """Persistent U, W, X reference blocks for steady-state spmmvm_fused timing
+        (timed reference arm / cpu_baseline): session.run(steps) -> seconds."""
+        ref = self
+        h = _vp()
+        self._chk(self.lib.ref_fused_session_create(m.h, width, C.byref(h)))
+
+        class _Session:
+            def run(self, steps, alpha=0.37, beta=0.0, coeff=0.25):
+                sec = _dbl()
+                ref._chk(ref.lib.ref_fused_session_run(h, steps, alpha, beta, coeff,
+                                                       C.byref(sec)))
+                return sec.value
+
+            def apply_filter(self, combined, alpha, beta):
+                comb = np.ascontiguousarray(combined, dtype=np.float64)
+                sec = _dbl()
+                ref._chk(ref.lib.ref_fused_session_apply(h, _ptr(comb), len(comb) - 1, alpha,
+                                                         beta, C.byref(sec)))
+                return sec.value
+
+            def gram(self):
+                sec = _dbl()
+                ref._chk(ref.lib.ref_fused_session_gram(h, C.byref(sec)))
+                return sec.value
+
+            def close(self):
+                if h.value:
+                    ref.lib.ref_fused_session_free(h)
+                    h.value = None
+
+            def __del__(self):
+                self.close()
+
+        return _Session()
 
     def svqb(self, y, drop_tol=1e-14):
         y = np.ascontiguousarray(y)

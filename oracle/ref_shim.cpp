@@ -408,6 +408,122 @@ int ref_time_fused_steps(void* h, int64_t width, int steps, double alpha, double
     });
 }
 
+// A persistent steady-state timing session for the CPU baseline: U, W, X blocks of the
+// reference's own BlockVector type allocated and filled once (a cheap deterministic
+// fill, touched in parallel so the pages are resident), then repeated calls timing
+// `steps` reference spmmvm_fused steps (kernels.hpp:74-118) with pointer swaps as
+// apply_filter's loop does (filter.hpp:105-114).  Timing infrastructure, not a kernel.
+struct FusedSession {
+    void* h = nullptr;
+    int64_t width = 0;
+    BlockVector<double> ru, rw, rx;
+    BlockVector<Complex> cu, cw, cx;
+};
+
+int ref_fused_session_create(void* h, int64_t width, void** out) {
+    return guard([&] {
+        auto s = std::make_unique<FusedSession>();
+        s->h = h;
+        s->width = width;
+        with_matrix(h, [&](const auto& a) {
+            using S = std::decay_t<decltype(a.values()[0])>;
+            auto fill = [&](BlockVector<S>& b, double phase) {
+                b = BlockVector<S>(a.dim(), width);
+                S* d = b.data();
+                const int64_t n = a.dim() * width;
+#pragma omp parallel for schedule(static)
+                for (int64_t i = 0; i < n; ++i) {
+                    const double v = std::sin(0.001 * static_cast<double>(i % 100003) + phase);
+                    if constexpr (std::is_same_v<S, Complex>)
+                        d[i] = Complex(v, 0.5 * v);
+                    else
+                        d[i] = v;
+                }
+            };
+            if constexpr (std::is_same_v<S, Complex>) {
+                fill(s->cu, 0.1);
+                fill(s->cw, 0.2);
+                fill(s->cx, 0.3);
+            } else {
+                fill(s->ru, 0.1);
+                fill(s->rw, 0.2);
+                fill(s->rx, 0.3);
+            }
+        });
+        *out = s.release();
+    });
+}
+
+int ref_fused_session_run(void* sess, int steps, double alpha, double beta, double coeff,
+                          double* seconds) {
+    return guard([&] {
+        auto* s = static_cast<FusedSession*>(sess);
+        with_matrix(s->h, [&](const auto& a) {
+            using S = std::decay_t<decltype(a.values()[0])>;
+            BlockVector<S>*pu, *pw, *px;
+            if constexpr (std::is_same_v<S, Complex>) {
+                pu = &s->cu; pw = &s->cw; px = &s->cx;
+            } else {
+                pu = &s->ru; pw = &s->rw; px = &s->rx;
+            }
+            const auto t0 = std::chrono::steady_clock::now();
+            for (int n = 0; n < steps; ++n) {
+                spmmvm_fused(a, *pu, *pw, *px, alpha, beta, coeff);
+                std::swap(pu, pw);
+            }
+            *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if constexpr (std::is_same_v<S, Complex>) {
+                if (pu != &s->cu) std::swap(s->cu, s->cw);
+            } else {
+                if (pu != &s->ru) std::swap(s->ru, s->rw);
+            }
+        });
+    });
+}
+
+// the reference's apply_filter (filter.hpp:73-116) on the session's X block, in place,
+// timed around the call alone (its own start-up allocations included)
+int ref_fused_session_apply(void* sess, const double* combined, int degree, double alpha,
+                            double beta, double* seconds) {
+    return guard([&] {
+        auto* s = static_cast<FusedSession*>(sess);
+        with_matrix(s->h, [&](const auto& a) {
+            using S = std::decay_t<decltype(a.values()[0])>;
+            BlockVector<S>* px;
+            if constexpr (std::is_same_v<S, Complex>)
+                px = &s->cx;
+            else
+                px = &s->rx;
+            auto p = filter_from(combined, degree, alpha, beta);
+            const auto t0 = std::chrono::steady_clock::now();
+            auto m = apply_filter(a, *px, p, false);
+            *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            (void)m;
+        });
+    });
+}
+
+// the reference's gram(X, X) (kernels.hpp:165-192) of the session's X block, timed
+int ref_fused_session_gram(void* sess, double* seconds) {
+    return guard([&] {
+        auto* s = static_cast<FusedSession*>(sess);
+        with_matrix(s->h, [&](const auto& a) {
+            using S = std::decay_t<decltype(a.values()[0])>;
+            const auto t0 = std::chrono::steady_clock::now();
+            if constexpr (std::is_same_v<S, Complex>) {
+                auto g = gram(s->cx, s->cx);
+                (void)g;
+            } else {
+                auto g = gram(s->rx, s->rx);
+                (void)g;
+            }
+            *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        });
+    });
+}
+
+void ref_fused_session_free(void* sess) { delete static_cast<FusedSession*>(sess); }
+
 // ---- solver pieces (solver.cpp) ----
 int ref_svqb(int kind, int64_t dim, int64_t width, const void* y, double drop_tol, void* q,
              int64_t* rank) {

@@ -137,6 +137,7 @@ _SIGS = {
     "chebfd_apply_filter_host": (_int, [_vp, _vp, _i64, _vp, _int, _dbl, _dbl, _vp]),
     "chebfd_filter_pipe_create": (_int, [_vp, _i64, _pp]),
     "chebfd_filter_pipe_submit": (_int, [_vp, _vp, _vp, _vp, _int, _dbl, _dbl]),
+    "chebfd_filter_pipe_submit_gram": (_int, [_vp, _vp, _vp, _vp, _int, _dbl, _dbl, _vp]),
     "chebfd_filter_pipe_wait": (_int, [_vp]),
     "chebfd_filter_pipe_destroy": (_int, [_vp]),
     "chebfd_svqb": (_int, [_vp, _dbl, _vp, _vp]),

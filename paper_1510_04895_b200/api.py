@@ -627,13 +627,27 @@ class FilterPipe:
         _check(_lib().chebfd_filter_pipe_create(A._h, self.width_, C.byref(self._h)))
         self._keep = []
 
-    def submit(self, x_in: np.ndarray, p: "FilterPolynomial", x_out: Optional[np.ndarray] = None):
+    def submit(self, x_in: np.ndarray, p: "FilterPolynomial", x_out: Optional[np.ndarray] = None,
+               gram_out: Optional[np.ndarray] = None):
+        """Queue one filter of x_in (result in x_out, default in place); with gram_out
+        (width x width, matrix dtype) also the Gram X^H X of the filtered block."""
         x_out = x_in if x_out is None else x_out
         for x in (x_in, x_out):
             if x.dtype != self.A.dtype or not x.flags.c_contiguous or x.shape != (self.A.local_rows, self.width_):
                 raise InvalidArgument("filter_pipe: host block must be C-contiguous "
                                       "(local rows x width) of the matrix dtype")
         comb = np.ascontiguousarray(p.combined, dtype=np.float64)
+        if p.degree >= 2 and len(comb) < p.degree + 1:
+            raise InvalidArgument("apply_filter: coefficient array shorter than degree+1")
+        if gram_out is not None:
+            if (gram_out.dtype != self.A.dtype or not gram_out.flags.c_contiguous
+                    or gram_out.shape != (self.width_, self.width_)):
+                raise InvalidArgument("filter_pipe: gram_out must be C-contiguous (width x width)")
+            self._keep.append((x_in, x_out, gram_out))
+            _check(_lib().chebfd_filter_pipe_submit_gram(self._h, _ptr(x_in), _ptr(x_out),
+                                                         _ptr(comb), p.degree, p.alpha, p.beta,
+                                                         _ptr(gram_out)))
+            return
         self._keep.append((x_in, x_out))
         _check(_lib().chebfd_filter_pipe_submit(self._h, _ptr(x_in), _ptr(x_out), _ptr(comb),
                                                 p.degree, p.alpha, p.beta))

@@ -9,6 +9,7 @@
 #include <complex>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -769,6 +770,26 @@ int chebfd_nccl_unique_id(unsigned char id[128]) {
     });
 }
 
+// One CUDA device per process (one process per GPU, torchrun-style): entry points launch
+// on the thread's current device and the kernel attribute / occupancy caches are keyed by
+// kernel only, so contexts on two devices in one process are refused.
+static std::mutex g_dev_mu;
+static int g_dev = -1, g_dev_ctxs = 0;
+
+static void claim_device(int device) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_dev_ctxs > 0 && g_dev != device)
+        fail(CHEBFD_ERR_UNSUPPORTED, "one CUDA device per process: contexts already exist on device " +
+                                         std::to_string(g_dev));
+    g_dev = device;
+    ++g_dev_ctxs;
+}
+
+static void release_device() {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_dev_ctxs > 0 && --g_dev_ctxs == 0) g_dev = -1;
+}
+
 static void ctx_init(Context& c, int device) {
     c.device = device;
     CFD_CUDA(cudaSetDevice(device));
@@ -796,9 +817,15 @@ static void ctx_init(Context& c, int device) {
 
 int chebfd_ctx_create(int device, chebfd_ctx** out) {
     return guard([&] {
-        auto c = std::make_unique<Context>();
-        ctx_init(*c, device);
-        *out = reinterpret_cast<chebfd_ctx*>(c.release());
+        claim_device(device);
+        try {
+            auto c = std::make_unique<Context>();
+            ctx_init(*c, device);
+            *out = reinterpret_cast<chebfd_ctx*>(c.release());
+        } catch (...) {
+            release_device();
+            throw;
+        }
     });
 }
 
@@ -806,24 +833,32 @@ int chebfd_ctx_create_dist(int device, int rank, int nranks, const unsigned char
                            chebfd_ctx** out) {
     return guard([&] {
         require(nranks >= 1 && rank >= 0 && rank < nranks, "ctx_create_dist: bad rank/nranks");
-        auto c = std::make_unique<Context>();
-        ctx_init(*c, device);
-        c->rank = rank;
-        c->nranks = nranks;
-        if (nranks > 1) {
-            ncclUniqueId u;
-            std::memcpy(u.internal, id, 128);
-            nccl_check(ncclCommInitRank(&c->nccl, nranks, u, rank), "ncclCommInitRank");
+        claim_device(device);
+        try {
+            auto c = std::make_unique<Context>();
+            ctx_init(*c, device);
+            c->rank = rank;
+            c->nranks = nranks;
+            if (nranks > 1) {
+                ncclUniqueId u;
+                std::memcpy(u.internal, id, 128);
+                nccl_check(ncclCommInitRank(&c->nccl, nranks, u, rank), "ncclCommInitRank");
+            }
+            *out = reinterpret_cast<chebfd_ctx*>(c.release());
+        } catch (...) {
+            release_device();
+            throw;
         }
-        *out = reinterpret_cast<chebfd_ctx*>(c.release());
     });
 }
 
 int chebfd_ctx_destroy(chebfd_ctx* ctx) {
     return guard([&] {
         Context* c = reinterpret_cast<Context*>(ctx);
-        if (c) cudaSetDevice(c->device);
+        if (!c) return;
+        cudaSetDevice(c->device);
         delete c;
+        release_device();
     });
 }
 
@@ -1371,6 +1406,7 @@ struct FilterPipe {
     Matrix* m = nullptr;
     int64_t width = 0;
     std::unique_ptr<Block> slot[2];
+    DeviceBuffer gram[2];  // per-slot device Gram of the filtered block (submit_gram)
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t in_ready[2] = {}, done[2] = {}, out_done[2] = {};
     bool used[2] = {false, false};
@@ -1410,12 +1446,33 @@ int chebfd_filter_pipe_create(chebfd_matrix* a, int64_t width, chebfd_filter_pip
     });
 }
 
+static void pipe_submit(FilterPipe& p, const void* host_in, void* host_out, const double* combined,
+                        int degree, double alpha, double beta, void* gram_host);
+
 int chebfd_filter_pipe_submit(chebfd_filter_pipe* pipe, const void* host_in, void* host_out,
                               const double* combined, int degree, double alpha, double beta) {
     return guard([&] {
         require(pipe != nullptr && host_in != nullptr && host_out != nullptr,
                 "filter_pipe_submit: null argument");
-        FilterPipe& p = *reinterpret_cast<FilterPipe*>(pipe);
+        pipe_submit(*reinterpret_cast<FilterPipe*>(pipe), host_in, host_out, combined, degree, alpha,
+                    beta, nullptr);
+    });
+}
+
+int chebfd_filter_pipe_submit_gram(chebfd_filter_pipe* pipe, const void* host_in, void* host_out,
+                                   const double* combined, int degree, double alpha, double beta,
+                                   void* gram_host) {
+    return guard([&] {
+        require(pipe != nullptr && host_in != nullptr && host_out != nullptr && gram_host != nullptr,
+                "filter_pipe_submit_gram: null argument");
+        pipe_submit(*reinterpret_cast<FilterPipe*>(pipe), host_in, host_out, combined, degree, alpha,
+                    beta, gram_host);
+    });
+}
+
+static void pipe_submit(FilterPipe& p, const void* host_in, void* host_out, const double* combined,
+                        int degree, double alpha, double beta, void* gram_host) {
+    {
         if (degree < 2) fail(CHEBFD_ERR_INVALID_ARGUMENT, "apply_filter: degree must be >= 2");
         Context& c = *p.c;
         const int s = p.next;
@@ -1427,12 +1484,22 @@ int chebfd_filter_pipe_submit(chebfd_filter_pipe* pipe, const void* host_in, voi
         CFD_CUDA(cudaEventRecord(p.in_ready[s], p.h2d));
         CFD_CUDA(cudaStreamWaitEvent(c.stream, p.in_ready[s], 0));
         apply_filter_device(c, *p.m, X, combined, degree, alpha, beta, nullptr);
+        const size_t gbytes = static_cast<size_t>(X.width * X.width) * X.scalar_bytes();
+        if (gram_host) {
+            // the Rayleigh-Ritz Gram X^H X of the filtered block (kernels.hpp:165-192),
+            // all-reduced over ranks, into the slot's device buffer
+            p.gram[s].ensure(gbytes);
+            gemm_gram(c, X, X, p.gram[s].p);
+            allreduce_sum(c, p.gram[s].as<double>(), gbytes / 8, c.stream);
+        }
         CFD_CUDA(cudaEventRecord(p.done[s], c.stream));
         CFD_CUDA(cudaStreamWaitEvent(p.d2h, p.done[s], 0));
         CFD_CUDA(cudaMemcpyAsync(host_out, X.owned(), X.owned_bytes(), cudaMemcpyDeviceToHost, p.d2h));
+        if (gram_host)
+            CFD_CUDA(cudaMemcpyAsync(gram_host, p.gram[s].p, gbytes, cudaMemcpyDeviceToHost, p.d2h));
         CFD_CUDA(cudaEventRecord(p.out_done[s], p.d2h));
         p.used[s] = true;
-    });
+    }
 }
 
 int chebfd_filter_pipe_wait(chebfd_filter_pipe* pipe) {
