@@ -106,7 +106,12 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
        CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12, CHEBFD_OPT_PDL = 14,
        CHEBFD_OPT_DELAYED_X = 15, CHEBFD_OPT_BAND_BYTES = 16, CHEBFD_OPT_ASYNC_START = 17,
-       CHEBFD_OPT_TILES_PER_CTA = 18 };
+       CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19 };
+/* CHEBFD_OPT_COMPACT_HALO (default 1; set before building distributed matrices): halos of
+ * structurally symmetric operators (the lattice models, bitwise-Hermitian from_csr input)
+ * hold only the neighbour rows the local rows reference -- TI reads orbitals {0,3} of the
+ * plane below and {1,2} of the plane above, half the plane -- packed on the sender by a
+ * gather kernel; 0 = whole contiguous neighbour planes. */
 /* CHEBFD_OPT_TILES_PER_CTA (default 2): band-ordered launches run a non-persistent grid
  * of this many consecutive tiles per CTA, dispatched in order by the hardware (a compact
  * wavefront; persistent CTA-strided grids drift apart and lose the band's L2 reuse);
@@ -136,6 +141,8 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
  * Chebyshev doubling identities T_2n = 2 T_n^2 - 1, T_2n+1 = 2 T_n T_n+1 - T_1: dots of
  * the recurrence vectors already in registers, no x0 stream, and only the first half of
  * the steps reduce (KPM: half the recurrence steps).  Equal up to rounding. */
+/* step launches that ran in the band tile order (CHEBFD_OPT_BAND_BYTES) so far */
+int chebfd_ctx_band_launches(chebfd_ctx* ctx, int64_t* count);
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */
@@ -476,6 +483,40 @@ int chebfd_solve_ex(chebfd_matrix* a, const chebfd_solver_options* opts, chebfd_
                     int cap, double* values, double* residual_norms, int* accepted,
                     double* history, chebfd_block** vectors, int weight_cap,
                     double* weight_moments, int* weight_len);
+
+/* ---- virtual rank groups (vgroup.cu) --------------------------------------------- */
+/* The distributed filter's nranks ranks (z-plane row partition, halos, interior /
+ * boundary launches, cross-launch dot reduction) driven in lockstep by one host thread
+ * on ONE device: rank r's halo rows are pulled from the neighbours' blocks by a gather
+ * kernel on its comm stream, ordered by events (no kernel waits on another), and the
+ * whole filter can be captured as one CUDA graph.  Results equal the single-rank
+ * path's bit for bit (row-local arithmetic); moments, dots and Gram matrices are summed
+ * over ranks in rank order.  Used to exercise and time the multi-rank device path where
+ * only one GPU exists.  Rank contexts come from chebfd_vgroup_context; blocks are
+ * created per rank from the rank's matrix (chebfd_block_create). */
+typedef struct chebfd_vgroup chebfd_vgroup;
+int chebfd_vgroup_create(int device, int nranks, chebfd_vgroup** out);
+int chebfd_vgroup_destroy(chebfd_vgroup* g);
+int chebfd_vgroup_context(chebfd_vgroup* g, int rank, chebfd_ctx** out);
+/* CHEBFD_OPT_GRAPHS: one graph for all ranks' steps; other options go to every rank */
+int chebfd_vgroup_set_option(chebfd_vgroup* g, int option, int64_t value);
+/* out[nranks]: rank r's partition of the lattice model (0 graphene, 1 TI) */
+int chebfd_vgroup_matrix_lattice(chebfd_vgroup* g, int model, const chebfd_lattice* spec,
+                                 chebfd_matrix** out);
+/* apply_filter over all ranks (a[r], x[r]); moments: (degree+1) x nb summed over ranks */
+int chebfd_vgroup_apply_filter(chebfd_vgroup* g, chebfd_matrix* const* a, chebfd_block* const* x,
+                               const double* combined, int degree, double alpha, double beta,
+                               double* moments);
+/* spmmvm_fused over all ranks; dots (Kahan per rank) summed over ranks */
+int chebfd_vgroup_spmmvm_fused(chebfd_vgroup* g, chebfd_matrix* const* a, chebfd_block* const* u,
+                               chebfd_block* const* w, chebfd_block* const* x, double alpha,
+                               double beta, double coeff, void* dots);
+/* gram(X, Y) summed over ranks */
+int chebfd_vgroup_gram(chebfd_vgroup* g, chebfd_block* const* x, chebfd_block* const* y,
+                       void* out);
+/* halo rows received (lo, hi) and rows sent (lo, hi) by a distributed matrix's rank */
+int chebfd_vgroup_halo_rows(chebfd_matrix* a, int64_t* halo_lo, int64_t* halo_hi,
+                            int64_t* send_lo, int64_t* send_hi);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ from .api import (  # noqa: F401
     optimize_degree, quality, host_randomize, read_matrix_market, write_matrix_market,
     save_block, load_block, BenchPoint, BenchReport, bandwidth_probe, bandwidth_probe_min_bytes,
     bench_filter, FilterPipe, host_array, experimental_build,
-    filter_schedule_bytes, WeightDensity, weight_density,
+    filter_schedule_bytes, WeightDensity, weight_density, VirtualGroup,
 )
 from ._lib import LIB_PATH, load  # noqa: F401
 

@@ -72,6 +72,15 @@ _SIGS = {
     "chebfd_last_error": (C.c_char_p, []),
     "chebfd_version": (C.c_char_p, []),
     "chebfd_build_features": (_int, []),
+    "chebfd_vgroup_create": (_int, [_int, _int, _pp]),
+    "chebfd_vgroup_destroy": (_int, [_vp]),
+    "chebfd_vgroup_context": (_int, [_vp, _int, _pp]),
+    "chebfd_vgroup_set_option": (_int, [_vp, _int, _i64]),
+    "chebfd_vgroup_matrix_lattice": (_int, [_vp, _int, _vp, _vp]),
+    "chebfd_vgroup_apply_filter": (_int, [_vp, _vp, _vp, _vp, _int, _dbl, _dbl, _vp]),
+    "chebfd_vgroup_spmmvm_fused": (_int, [_vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp]),
+    "chebfd_vgroup_gram": (_int, [_vp, _vp, _vp, _vp]),
+    "chebfd_vgroup_halo_rows": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "chebfd_nccl_unique_id": (_int, [_vp]),
     "chebfd_ctx_create": (_int, [_int, _pp]),
     "chebfd_ctx_create_dist": (_int, [_int, _int, _int, _vp, _pp]),
@@ -81,6 +90,7 @@ _SIGS = {
     "chebfd_ctx_info": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "chebfd_ctx_launch_count": (_int, [_vp, _vp]),
     "chebfd_ctx_set_option": (_int, [_vp, _int, _i64]),
+    "chebfd_ctx_band_launches": (_int, [_vp, _vp]),
     "chebfd_ctx_event_record": (_int, [_vp, _int]),
     "chebfd_ctx_event_elapsed": (_int, [_vp, _int, _int, _vp]),
     "chebfd_host_alloc": (_int, [C.c_size_t, _pp]),

@@ -88,9 +88,10 @@ class Context:
     parallel.hpp:18-54).  ``Context.distributed(rank, nranks, uid)`` joins a
     row-partitioned multi-GPU context (one process per GPU)."""
 
-    def __init__(self, device: int = 0, _handle=None):
+    def __init__(self, device: int = 0, _handle=None, _borrowed=False):
         self._h = C.c_void_p()
         self._children = weakref.WeakSet()  # matrices / blocks to release first
+        self._borrowed = _borrowed  # a virtual group's rank context: the group destroys it
         if _handle is None:
             _check(_lib().chebfd_ctx_create(device, C.byref(self._h)))
         else:
@@ -121,7 +122,8 @@ class Context:
                     k.close()
             for k in kids:
                 k.close()
-            _lib().chebfd_ctx_destroy(self._h)
+            if not self._borrowed:
+                _lib().chebfd_ctx_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):
@@ -150,6 +152,13 @@ class Context:
         _check(_lib().chebfd_ctx_launch_count(self._h, C.byref(v)))
         return v.value
 
+    @property
+    def band_launches(self) -> int:
+        """Step launches that ran in the band (2.5D) tile order."""
+        v = C.c_int64()
+        _check(_lib().chebfd_ctx_band_launches(self._h, C.byref(v)))
+        return v.value
+
     def record(self, slot: int):
         """Record CUDA event `slot` (0..15) on the context stream."""
         _check(_lib().chebfd_ctx_event_record(self._h, slot))
@@ -168,7 +177,8 @@ class Context:
         code = {"graphs": 1, "overlap": 2, "kernel": 3, "slab_units": 5, "pair": 6,
                 "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
                 "pair_slab": 11, "moments": 12, "pdl": 14, "delayed_x": 15,
-                "band_bytes": 16, "async_start": 17, "tiles_per_cta": 18}[name]
+                "band_bytes": 16, "async_start": 17, "tiles_per_cta": 18,
+                "compact_halo": 19}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):
@@ -269,6 +279,90 @@ def _csr(fn, spec, r0, r1, dtype):
     vals = np.empty(nnz.value, dtype)
     _check(fn(C.byref(s), r0, r1, C.byref(dim), C.byref(nnz), _ptr(offs), _ptr(cols), _ptr(vals)))
     return offs, cols, vals
+
+
+# --------------------------------------------------------- virtual ranks --
+class VirtualGroup:
+    """The distributed filter's ranks on ONE GPU (chebfd_vgroup_*, vgroup.cu): each rank
+    a Context with its row partition and halos, all ranks' steps enqueued in lockstep
+    with the halo rows pulled from the neighbours' blocks (optionally one CUDA graph).
+    Results equal the single-rank path's bits; dots / moments / Gram summed over ranks."""
+
+    def __init__(self, nranks: int, device: int = 0):
+        self._h = C.c_void_p()
+        _check(_lib().chebfd_vgroup_create(device, nranks, C.byref(self._h)))
+        self.nranks = nranks
+        self.ranks = []
+        for r in range(nranks):
+            h = C.c_void_p()
+            _check(_lib().chebfd_vgroup_context(self._h, r, C.byref(h)))
+            self.ranks.append(Context(_handle=h, _borrowed=True))
+
+    def set_option(self, name: str, value):
+        code = {"graphs": 1}.get(name)
+        if code is not None:
+            _check(_lib().chebfd_vgroup_set_option(self._h, code, int(value)))
+            return
+        for c in self.ranks:
+            c.set_option(name, value)
+
+    def _lattice(self, model, spec):
+        hs = (C.c_void_p * self.nranks)()
+        s = spec._c()
+        _check(_lib().chebfd_vgroup_matrix_lattice(self._h, model, C.byref(s), hs))
+        return [SparseMatrix(self.ranks[r], C.c_void_p(hs[r])) for r in range(self.nranks)]
+
+    def topological_insulator(self, spec: "LatticeSpec"):
+        return self._lattice(1, spec)
+
+    def graphene(self, spec: "LatticeSpec"):
+        return self._lattice(0, spec)
+
+    @staticmethod
+    def _arr(objs):
+        a = (C.c_void_p * len(objs))()
+        for i, o in enumerate(objs):
+            a[i] = o._h.value
+        return a
+
+    def apply_filter(self, As, Xs, p: "FilterPolynomial", want_moments=False):
+        comb = np.ascontiguousarray(p.combined, dtype=np.float64)
+        nb = Xs[0].width_
+        mom = np.empty((p.degree + 1, nb)) if want_moments else None
+        _check(_lib().chebfd_vgroup_apply_filter(self._h, self._arr(As), self._arr(Xs), _ptr(comb),
+                                                 p.degree, p.alpha, p.beta, _ptr(mom)))
+        return MomentTable(p.degree, nb, mom) if want_moments else None
+
+    def spmmvm_fused(self, As, Us, Ws, Xs, alpha, beta, coeff, dots=False):
+        d = np.empty(Us[0].width_, dtype=Us[0].dtype) if dots else None
+        _check(_lib().chebfd_vgroup_spmmvm_fused(self._h, self._arr(As), self._arr(Us),
+                                                 self._arr(Ws), self._arr(Xs), alpha, beta, coeff,
+                                                 _ptr(d)))
+        return d
+
+    def gram(self, Xs, Ys):
+        g = np.empty((Xs[0].width_, Ys[0].width_), dtype=Xs[0].dtype)
+        _check(_lib().chebfd_vgroup_gram(self._h, self._arr(Xs), self._arr(Ys), _ptr(g)))
+        return g
+
+    @staticmethod
+    def halo_rows(A):
+        v = [C.c_int64() for _ in range(4)]
+        _check(_lib().chebfd_vgroup_halo_rows(A._h, *[C.byref(x) for x in v]))
+        return dict(halo_lo=v[0].value, halo_hi=v[1].value, send_lo=v[2].value, send_hi=v[3].value)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            for c in self.ranks:
+                c.close()
+            _lib().chebfd_vgroup_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ----------------------------------------------------------- sparse matrix --

@@ -236,6 +236,7 @@ AsyncRandomize::~AsyncRandomize() {
 void ctx_sync(Context& c) { CFD_CUDA(cudaStreamSynchronize(c.stream)); }
 
 void purge_graphs(Context& c, const void* a, const void* x) {
+    if (c.vgroup) vgroup_purge(*c.vgroup, a, x);
     for (auto it = c.graphs.begin(); it != c.graphs.end();) {
         if ((a && it->first.a == a) || (x && it->first.x == x)) {
             cudaGraphExecDestroy(it->second.exec);
@@ -310,6 +311,16 @@ const void* gather_base(const Matrix& a, const Block& b) {
 // Message order per rank: send A (my last rows -> hi's lo halo), send B (my
 // first rows -> lo's hi halo), recv A (lo halo), recv B (hi halo); this
 // matches in order even when lo and hi are the same peer (2-rank ring).
+// Compact halos first gather the sent rows into contiguous pack buffers (one small kernel
+// per side on `st`); the receiver's halo region is contiguous either way.
+void ensure_halo_buffers(Context& c, Matrix& a, int64_t width) {
+    const Partition& p = a.part;
+    if (!p.compact || c.nranks == 1) return;
+    const size_t rb = static_cast<size_t>(width) * (a.kind ? 16 : 8);
+    a.pack_lo.ensure(std::max<size_t>(p.send_lo_n * rb, 16));
+    a.pack_hi.ensure(std::max<size_t>(p.send_hi_n * rb, 16));
+}
+
 void exchange_halo(Context& c, const Matrix& a, Block& b, cudaStream_t st) {
     if (c.nranks == 1 || !c.nccl) return;
     const Partition& p = a.part;
@@ -317,13 +328,33 @@ void exchange_halo(Context& c, const Matrix& a, Block& b, cudaStream_t st) {
     const size_t words = row_bytes / 8;
     char* own = static_cast<char*>(b.owned());
     char* base = static_cast<char*>(const_cast<void*>(gather_base(a, b)));
+    const char* send_hi = own + p.send_hi_begin * row_bytes;
+    const char* send_lo = own + p.send_lo_begin * row_bytes;
+    if (p.compact) {
+        Matrix& am = const_cast<Matrix&>(a);
+        if (am.pack_hi.bytes < p.send_hi_n * row_bytes || am.pack_lo.bytes < p.send_lo_n * row_bytes) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            CFD_CUDA(cudaStreamIsCapturing(st, &cs));
+            if (cs != cudaStreamCaptureStatusNone)
+                fail(CHEBFD_ERR_RUNTIME, "halo pack buffers not sized before graph capture");
+            ensure_halo_buffers(c, am, b.width);
+        }
+        if (p.hi_rank >= 0 && p.send_hi_n > 0)
+            launch_gather_rows(c, am.pack_hi.p, own, am.send_hi_idx.as<int64_t>(), p.send_hi_n,
+                               static_cast<int64_t>(row_bytes), st);
+        if (p.lo_rank >= 0 && p.send_lo_n > 0)
+            launch_gather_rows(c, am.pack_lo.p, own, am.send_lo_idx.as<int64_t>(), p.send_lo_n,
+                               static_cast<int64_t>(row_bytes), st);
+        send_hi = static_cast<const char*>(am.pack_hi.p);
+        send_lo = static_cast<const char*>(am.pack_lo.p);
+    }
     nccl_check(ncclGroupStart(), "ncclGroupStart");
     if (p.hi_rank >= 0 && p.send_hi_n > 0)
-        nccl_check(ncclSend(own + p.send_hi_begin * row_bytes, p.send_hi_n * words, ncclFloat64,
-                            p.hi_rank, c.nccl, st), "ncclSend");
+        nccl_check(ncclSend(send_hi, p.send_hi_n * words, ncclFloat64, p.hi_rank, c.nccl, st),
+                   "ncclSend");
     if (p.lo_rank >= 0 && p.send_lo_n > 0)
-        nccl_check(ncclSend(own + p.send_lo_begin * row_bytes, p.send_lo_n * words, ncclFloat64,
-                            p.lo_rank, c.nccl, st), "ncclSend");
+        nccl_check(ncclSend(send_lo, p.send_lo_n * words, ncclFloat64, p.lo_rank, c.nccl, st),
+                   "ncclSend");
     if (p.lo_rank >= 0 && p.halo_lo > 0)
         nccl_check(ncclRecv(base, p.halo_lo * words, ncclFloat64, p.lo_rank, c.nccl, st),
                    "ncclRecv");
@@ -359,6 +390,8 @@ void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
     s.width_cols = gathered.width;
     s.in = gather_base(a, gathered);
     const Partition& p = a.part;
+    if (c.vgroup && (p.halo_lo || p.halo_hi))
+        fail(CHEBFD_ERR_UNSUPPORTED, "a virtual-group rank's halo needs the chebfd_vgroup_* entry points");
     if (c.nranks == 1 || !c.nccl || (p.halo_lo == 0 && p.halo_hi == 0)) {
         s.row0 = 0;
         s.row1 = p.local;
@@ -373,6 +406,14 @@ void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
     CFD_CUDA(cudaStreamWaitEvent(c.comm_stream, c.ev_a, 0));
     exchange_halo(c, a, gathered, c.comm_stream);
     CFD_CUDA(cudaEventRecord(c.ev_b, c.comm_stream));
+    launch_split(c, a, s);
+}
+
+// The step's launches once its halo exchange is enqueued on the comm stream and c.ev_b
+// marks its completion: interior rows (no halo reads) concurrently with the exchange,
+// then the boundary rows; the dot partials of the 2-3 launches are reduced by the last.
+void launch_split(Context& c, const Matrix& a, StepArgs s) {
+    const Partition& p = a.part;
     int used = 0, base = 0;
     // dot partials of column-slabbed launches cannot be split over interior and boundary
     // launches: such steps wait for the halo and run as one launch per slab
@@ -429,8 +470,9 @@ void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
 // (ring distance decides lo vs hi), then tell every rank what its
 // neighbours need from it.
 void setup_partition(Context& c, Matrix& m, const HostCsr& csr, int64_t r0, int64_t r1,
-                     const std::vector<int64_t>& starts) {
-    m.part = plan_rows(csr, r0, r1, starts);
+                     const std::vector<int64_t>& starts, bool compact) {
+    m.part = compact && c.nranks > 1 ? plan_rows_compact(csr, r0, r1, starts)
+                                     : plan_rows(csr, r0, r1, starts);
     Partition& p = m.part;
     const int P = c.nranks;
     // what do the neighbours need from me?  all-gather (halo_lo, halo_hi, lo_rank, hi_rank)
@@ -452,29 +494,56 @@ void setup_partition(Context& c, Matrix& m, const HostCsr& csr, int64_t r0, int6
 }
 
 std::unique_ptr<Matrix> matrix_from_host_csr(Context& c, const HostCsr& csr, int64_t r0, int64_t r1,
-                                             const std::vector<int64_t>& starts, int64_t nnz_global) {
+                                             const std::vector<int64_t>& starts, int64_t nnz_global,
+                                             bool symmetric) {
     auto m = std::make_unique<Matrix>();
     m->ctx = &c;
     m->kind = csr.kind;
     m->nnz_local = static_cast<int64_t>(csr.cols.size());
     m->nnz_global = nnz_global;
-    setup_partition(c, *m, csr, r0, r1, starts);
+    setup_partition(c, *m, csr, r0, r1, starts, symmetric && c.compact_halo);
+    build_matrix_device(c, *m, csr);
+    return m;
+}
+
+// Upload this rank's CSR (columns pre-mapped to extended rows for compact halos) and
+// convert it to SELL on the device; upload the compact halo send lists.
+void build_matrix_device(Context& c, Matrix& mat, const HostCsr& csr) {
+    Matrix* m = &mat;
+    const Partition& part = m->part;
+    const int64_t rows = part.local, nnz = m->nnz_local;
+    std::vector<int64_t> mapped;
+    const int64_t* cols_h = csr.cols.data();
+    if (part.compact) {
+        mapped.resize(csr.cols.size());
+        for (size_t q = 0; q < csr.cols.size(); ++q) {
+            mapped[q] = map_column(part, csr.cols[q]);
+            if (mapped[q] < 0) fail(CHEBFD_ERR_UNSUPPORTED, "matrix column outside this rank's rows and halos");
+        }
+        cols_h = mapped.data();
+        auto up = [&](DeviceBuffer& d, const std::vector<int64_t>& v) {
+            d.ensure(sizeof(int64_t) * std::max<size_t>(v.size(), 1));
+            if (!v.empty())
+                CFD_CUDA(cudaMemcpyAsync(d.p, v.data(), sizeof(int64_t) * v.size(),
+                                         cudaMemcpyHostToDevice, c.stream));
+        };
+        up(m->send_lo_idx, part.send_lo_rows);
+        up(m->send_hi_idx, part.send_hi_rows);
+    }
     // upload the CSR of owned rows and convert on the device
-    const int64_t rows = r1 - r0, nnz = m->nnz_local;
     DeviceBuffer d_offs(sizeof(int64_t) * (rows + 1));
     DeviceBuffer d_cols(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
     DeviceBuffer d_vals((csr.kind ? 16 : 8) * std::max<int64_t>(nnz, 1));
     CFD_CUDA(cudaMemcpyAsync(d_offs.p, csr.offs.data(), sizeof(int64_t) * (rows + 1),
                              cudaMemcpyHostToDevice, c.stream));
     if (nnz) {
-        CFD_CUDA(cudaMemcpyAsync(d_cols.p, csr.cols.data(), sizeof(int64_t) * nnz,
+        CFD_CUDA(cudaMemcpyAsync(d_cols.p, cols_h, sizeof(int64_t) * nnz,
                                  cudaMemcpyHostToDevice, c.stream));
         CFD_CUDA(cudaMemcpyAsync(d_vals.p, csr.vals.data(), sizeof(double) * csr.vals.size(),
                                  cudaMemcpyHostToDevice, c.stream));
     }
     build_sell(c, *m, d_offs.as<int64_t>(), d_cols.as<int64_t>(), d_vals.p, c.stream);
     ctx_sync(c);
-    return m;
 }
 
 int64_t allreduce_count(Context& c, int64_t v) {
@@ -495,8 +564,10 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
     const int64_t r0 = starts[c.rank], r1 = starts[c.rank + 1];
     HostCsr csr = ti ? gen_topological_insulator(s, r0, r1) : gen_graphene(s, r0, r1);
     const int64_t nnz_g = allreduce_count(c, static_cast<int64_t>(csr.cols.size()));
-    auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g);
-    m->hermitian = true;  // both models add every hopping with its conjugate (models.cpp:80-178)
+    // both models add every hopping with its conjugate (models.cpp:80-178): Hermitian,
+    // hence structurally symmetric (compact halos apply)
+    auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g, true);
+    m->hermitian = true;
     if (ti) {  // row = 4 (x + Lx (y + Ly z)) + orbital (models.hpp:15-19)
         m->plane_rows = 4 * s.lx * s.ly;
         m->line_rows = 4 * s.lx;
@@ -547,6 +618,14 @@ bool moment_doubling(const Context& c, const Matrix& a) { return c.moments_mode 
 
 void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double alpha, double beta,
                     const double* coeff_dev, double* mom_dev, FilterWorkspace& ws) {
+    enqueue_filter(c, a, x, degree, alpha, beta, coeff_dev, mom_dev, ws,
+                   [&](const StepArgs& s, Block& g) { run_step_all(c, a, s, g); });
+    if (mom_dev) allreduce_sum(c, mom_dev, static_cast<size_t>((degree + 1) * x.width), c.stream);
+}
+
+void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double alpha, double beta,
+                    const double* coeff_dev, double* mom_dev, FilterWorkspace& ws,
+                    const std::function<void(const StepArgs&, Block&)>& run) {
     const bool moments = mom_dev != nullptr;
     // doubling (DMODE 4): step n's registers give the raw sums of moments 2n-2, 2n-1, so
     // only steps n <= degree/2 + 1 reduce and no x0 copy is kept (mom_dev has 2 spare rows)
@@ -561,7 +640,7 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     s.beta = beta;
     s.dots_mode = moments ? (dbl ? 4 : 3) : 0;
     s.dots_out = mom_dev;
-    run_step_all(c, a, s, x);
+    run(s, x);
     // w = 2(alpha A + beta)u - x;  x = g0c0 x + g1c1 u + g2c2 w   [+ m2 = <x0,w>; doubling:
     // raw <u,u>, <u,w> for m2, m3]
     StepArgs s2{};
@@ -573,7 +652,7 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
     s2.coeff_dev = coeff_dev;
     s2.dots_mode = moments ? (dbl ? 4 : 2) : 0;
     s2.dots_out = moments ? mom_dev + 2 * nb : nullptr;
-    run_step_all(c, a, s2, *ws.u);
+    run(s2, *ws.u);
     Block* pu = ws.u.get();
     Block* pw = ws.w.get();
     // delayed X update (CHEBFD_OPT_DELAYED_X = G): of each group of G steps the first G-1 run
@@ -639,9 +718,8 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
         f.coeff_index = n;
         f.dots_mode = dmode;
         f.dots_out = dmode ? mom_dev + mrow * nb : nullptr;
-        run_step_all(c, a, f, *pu);
+        run(f, *pu);
     }
-    if (moments) allreduce_sum(c, mom_dev, static_cast<size_t>((degree + 1) * nb), c.stream);
 }
 
 void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* combined, int degree,
@@ -653,6 +731,7 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
     const int64_t nb = x.width;
     FilterWorkspace& ws = filter_workspace(c, a, nb, moments && !dbl);
     Matrix& am = const_cast<Matrix&>(a);
+    ensure_halo_buffers(c, am, nb);
     if (c.kernel_variant >= 1) {  // pre-scaled values for the start step (alpha) and 2 alpha steps
         ensure_scaled_values(c, am, alpha, c.stream);
         ensure_scaled_values(c, am, 2.0 * alpha, c.stream);
@@ -815,6 +894,35 @@ static void ctx_init(Context& c, int device) {
     ctx_sync(c);
 }
 
+}  // extern "C"
+
+namespace cfd {
+// contexts of a virtual rank group (vgroup.cu): same device, no NCCL communicator
+Context* create_group_context(int device, int rank, int nranks) {
+    claim_device(device);
+    try {
+        auto c = std::make_unique<Context>();
+        ctx_init(*c, device);
+        c->rank = rank;
+        c->nranks = nranks;
+        return c.release();
+    } catch (...) {
+        release_device();
+        throw;
+    }
+}
+
+void destroy_group_context(Context* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    delete c;
+    release_device();
+}
+
+}  // namespace cfd
+
+extern "C" {
+
 int chebfd_ctx_create(int device, chebfd_ctx** out) {
     return guard([&] {
         claim_device(device);
@@ -884,6 +992,10 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count) {
     return guard([&] { *count = reinterpret_cast<Context*>(ctx)->launches; });
 }
 
+int chebfd_ctx_band_launches(chebfd_ctx* ctx, int64_t* count) {
+    return guard([&] { *count = reinterpret_cast<Context*>(ctx)->band_launches; });
+}
+
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
     return guard([&] {
         Context* c = reinterpret_cast<Context*>(ctx);
@@ -917,6 +1029,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->band_bytes = value;
         else if (option == CHEBFD_OPT_ASYNC_START)
             c->async_start_entries = value;
+        else if (option == CHEBFD_OPT_COMPACT_HALO)
+            c->compact_halo = value != 0;
         else if (option == CHEBFD_OPT_TILES_PER_CTA)
             c->tiles_per_cta = static_cast<int>(std::max<int64_t>(value, 0));
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)
@@ -1022,8 +1136,9 @@ int chebfd_matrix_from_csr(chebfd_ctx* ctx, int kind, int64_t dim, const int64_t
         const int f = kind ? 2 : 1;
         const double* v = static_cast<const double*>(vals);
         h.vals.assign(v + f * offs[r0], v + f * offs[r1]);
-        auto m = matrix_from_host_csr(c, h, r0, r1, starts, nnz);
-        m->hermitian = csr_is_hermitian(kind, dim, offs, cols, v);
+        const bool herm = csr_is_hermitian(kind, dim, offs, cols, v);
+        auto m = matrix_from_host_csr(c, h, r0, r1, starts, nnz, herm);
+        m->hermitian = herm;
         *out = reinterpret_cast<chebfd_matrix*>(m.release());
     });
 }

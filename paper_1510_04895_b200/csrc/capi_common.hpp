@@ -1,6 +1,7 @@
 // Helpers shared by the C-ABI translation units (capi.cu, solver.cu, blas.cu).
 #pragma once
 #include <exception>
+#include <functional>
 #include <thread>
 
 #include <string>
@@ -56,6 +57,26 @@ void check_conforms(const Matrix& a, const Block& x, const char* who);
 // moments by the Chebyshev doubling identities (CHEBFD_OPT_MOMENTS, Hermitian operators)
 bool moment_doubling(const Context& c, const Matrix& a);
 void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered);
+// interior + boundary launches of a step whose halo exchange is enqueued (c.ev_b)
+void launch_split(Context& c, const Matrix& a, StepArgs s);
+const void* gather_base(const Matrix& a, const Block& b);
+void ensure_halo_buffers(Context& c, Matrix& a, int64_t width);
+void build_matrix_device(Context& c, Matrix& m, const HostCsr& csr);
+Context* create_group_context(int device, int rank, int nranks);
+struct VGroup;
+void vgroup_purge(VGroup& g, const void* a, const void* x);
+void destroy_group_context(Context* c);
+void setup_partition(Context& c, Matrix& m, const HostCsr& csr, int64_t r0, int64_t r1,
+                     const std::vector<int64_t>& starts, bool compact);
+void ensure_scaled_values(Context& ctx, Matrix& a, double s, cudaStream_t st);
+void purge_graphs(Context& c, const void* a, const void* x);
+struct FilterWorkspace;
+FilterWorkspace& filter_workspace(Context& c, const Matrix& a, int64_t width, bool moments);
+bool moment_doubling(const Context& c, const Matrix& a);
+// apply_filter's step sequence (filter.hpp:73-116) as calls run(step args, gathered block)
+void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double alpha, double beta,
+                    const double* coeff_dev, double* mom_dev, FilterWorkspace& ws,
+                    const std::function<void(const StepArgs&, Block&)>& run);
 void allreduce_sum(Context& c, double* dev, size_t n, cudaStream_t st);
 void column_dots_host(Context& c, const Block& x, const Block& y, void* out);
 void gram_host(Context& c, const Block& x, const Block& y, void* out);

@@ -69,6 +69,14 @@ struct Partition {
     // (local index) to lo_rank and [send_hi_begin, +send_hi_n) to hi_rank
     int64_t send_lo_begin = 0, send_lo_n = 0, send_hi_begin = 0, send_hi_n = 0;
     int64_t ext_rows() const { return halo_lo + local + halo_hi; }
+    // Compact halos (structurally symmetric operators, e.g. the lattice models): only the
+    // neighbour rows the local rows actually reference are exchanged -- TI reads orbitals
+    // {0,3} of the plane below and {1,2} of the plane above, half of each plane.  The
+    // halo regions then hold halo_lo_rows / halo_hi_rows (sorted global rows) in order,
+    // and this rank sends its rows send_lo_rows / send_hi_rows (sorted local indices).
+    // By structural symmetry a neighbour's halo list equals our send list to it.
+    bool compact = false;
+    std::vector<int64_t> halo_lo_rows, halo_hi_rows, send_lo_rows, send_hi_rows;
 };
 
 // Extended-row index of global column g in a partition (-2: not held).  Used
@@ -129,6 +137,10 @@ struct Matrix {
     // line (TI: 4 Lx Ly and 4 Lx); the step kernels' band tile order uses it
     int64_t plane_rows = 0, line_rows = 0;
     DeviceBuffer pair_sync; // pair kernel: item / exit tickets + per-1024-row group counters (zeroed)
+    // compact halos: this rank's rows sent to lo / hi (local indices, device), the pack
+    // buffers they are gathered into before ncclSend, and -- virtual groups -- the
+    // neighbours' local indices of this rank's halo rows (pulled by a gather kernel)
+    DeviceBuffer send_lo_idx, send_hi_idx, pack_lo, pack_hi, recv_lo_src, recv_hi_src;
 };
 
 // ---- block vector -------------------------------------------------------------------
@@ -191,6 +203,7 @@ struct Context {
     int kernel_variant = 1;  // step kernel: 0 register gathers, 1 TMA-staged matrix chunks,
                              // 2 TMA-staged matrix chunks + gathered rows (where a plan fits)
     int64_t launches = 0;
+    int64_t band_launches = 0;  // step launches that ran in the band (2.5D) tile order
     int slab_units = 0;   // step kernel column-slab width in 16-byte units (0: up to 256)
     // two fused steps per launch (pair.cu): 0 off, 1 where the wavefront's working set
     // fits the L2, 2 wherever the kernel applies; tuning knobs (0 / -1: automatic)
@@ -217,6 +230,10 @@ struct Context {
     // step launches without dots: non-persistent grids of this many consecutive row tiles
     // per CTA (0: persistent CTA-strided grids everywhere); CHEBFD_OPT_TILES_PER_CTA
     int tiles_per_cta = 2;
+    // exchange only the referenced halo rows of structurally symmetric operators (lattice
+    // models, bitwise-Hermitian from_csr input); CHEBFD_OPT_COMPACT_HALO
+    bool compact_halo = true;
+    struct VGroup* vgroup = nullptr;  // virtual rank group this context belongs to (vgroup.cu)
     DeviceBuffer dscratch;   // small device results (dots, Gram, moments)
     DeviceBuffer workspace;  // cuSOLVER / misc
     DeviceBuffer devinfo;
@@ -302,6 +319,9 @@ void launch_axpy_scalar(Context& ctx, Block& w, const Block& q, double hr, doubl
 void launch_copy_columns(Context& ctx, Block& dst, int64_t d0, const Block& src, int64_t s0,
                          int64_t n, cudaStream_t st);
 void launch_philox_normal(Context& ctx, Block& b, uint64_t seed, cudaStream_t st);
+// dst row i = src row idx[i] (device index list), rows of row_bytes
+void launch_gather_rows(Context& ctx, void* dst, const void* src, const int64_t* idx, int64_t n,
+                        int64_t row_bytes, cudaStream_t st);
 // SELL build from a device CSR (global column indices -> extended-row index)
 void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d_cols,
                 const void* d_vals, cudaStream_t st);
@@ -346,6 +366,12 @@ struct HostCsr;
 // Halos of rows [r0, r1) derived from the global columns they read (ring
 // distance decides lower vs upper neighbour); starts[q] = first row of rank q.
 Partition plan_rows(const HostCsr& csr, int64_t r0, int64_t r1, const std::vector<int64_t>& starts);
+// The same partition with compact halo lists (see Partition::compact).
+Partition plan_rows_compact(const HostCsr& csr, int64_t r0, int64_t r1,
+                            const std::vector<int64_t>& starts);
+// Extended-row index of global column g under a partition (compact lists searched),
+// -2 if the rank holds no copy.
+int64_t map_column(const Partition& p, int64_t g);
 // Send ranges from every rank's (halo_lo, halo_hi, lo_rank, hi_rank) (all4).
 void plan_sends(Partition& p, int rank, int nranks, const int64_t* all4);
 // filter design (design.cpp, restating filter_design.cpp)

@@ -52,6 +52,27 @@ __global__ void scale_values_kernel(double* __restrict__ out, const double* __re
         out[i] = mul(in[i], s);
 }
 
+// dst row i = src row idx[i] (rows of `words` doubles): the compact halo's send-side pack
+// and the virtual group's pull of a neighbour's rows
+__global__ void gather_rows_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                   const int64_t* __restrict__ idx, int64_t n, int64_t words) {
+    const int64_t tot = n * words;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / words, k = i - r * words;
+        dst[i] = __ldg(&src[__ldg(&idx[r]) * words + k]);
+    }
+}
+__global__ void gather_rows2_kernel(double2* __restrict__ dst, const double2* __restrict__ src,
+                                    const int64_t* __restrict__ idx, int64_t n, int64_t units) {
+    const int64_t tot = n * units;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / units, k = i - r * units;
+        dst[i] = __ldg(&src[__ldg(&idx[r]) * units + k]);
+    }
+}
+
 // ---- generic per-column reductions ------------------------------------------------------
 // mode 0: out_S[k] = sum conj(x) y;  mode 1: out_d[k] = sum |av - lam v|^2
 template <bool CPLX, class T, int MODE>
@@ -420,6 +441,23 @@ void launch_scale_columns(Context& ctx, Block& b, const double* d_dev, cudaStrea
     ctx.launches++;
 }
 
+void launch_gather_rows(Context& ctx, void* dst, const void* src, const int64_t* idx, int64_t n,
+                        int64_t row_bytes, cudaStream_t st) {
+    if (n == 0 || row_bytes == 0) return;
+    const int64_t tot = n * row_bytes / 8;
+    const int grid = static_cast<int>(std::min<int64_t>((tot + 255) / 256, ctx.num_sms * 8));
+    if (row_bytes % 16 == 0)
+        gather_rows2_kernel<<<grid, 256, 0, st>>>(static_cast<double2*>(dst),
+                                                  static_cast<const double2*>(src), idx, n,
+                                                  row_bytes / 16);
+    else
+        gather_rows_kernel<<<grid, 256, 0, st>>>(static_cast<double*>(dst),
+                                                 static_cast<const double*>(src), idx, n,
+                                                 row_bytes / 8);
+    CFD_CUDA(cudaGetLastError());
+    ctx.launches++;
+}
+
 void launch_copy_columns(Context& ctx, Block& dst, int64_t d0, const Block& src, int64_t s0,
                          int64_t n, cudaStream_t st) {
     const int f = dst.kind ? 2 : 1;
@@ -478,7 +516,8 @@ void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d
         fail(CHEBFD_ERR_UNSUPPORTED, "extended row count exceeds int32 column indices");
     m.cols.ensure(sizeof(int) * std::max<int64_t>(entries, 1));
     m.vals.ensure((m.kind ? 16 : 8) * std::max<int64_t>(entries, 1));
-    const ColMap cm = colmap_of(m.part);
+    // compact halos: the host already mapped the columns to extended rows (identity map)
+    const ColMap cm = m.part.compact ? ColMap{0, m.part.ext_rows(), 0, 0, 0, 0} : colmap_of(m.part);
     const int64_t threads = m.nchunks * kChunk;
     if (threads > 0) {
         const unsigned grid = static_cast<unsigned>((threads + 255) / 256);

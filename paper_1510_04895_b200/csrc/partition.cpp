@@ -66,7 +66,75 @@ Partition plan_rows(const HostCsr& csr, int64_t r0, int64_t r1, const std::vecto
     return p;
 }
 
+Partition plan_rows_compact(const HostCsr& csr, int64_t r0, int64_t r1,
+                            const std::vector<int64_t>& starts) {
+    Partition p = plan_rows(csr, r0, r1, starts);
+    const int64_t D = csr.dim;
+    std::vector<int64_t> lo, hi, slo, shi;
+    for (int64_t i = 0; i < p.local; ++i) {
+        bool to_lo = false, to_hi = false;
+        for (int64_t q = csr.offs[i]; q < csr.offs[i + 1]; ++q) {
+            const int64_t g = csr.cols[q];
+            if (g >= r0 && g < r1) continue;
+            const int64_t up = ((g - r1) % D + D) % D;
+            const int64_t dn = ((r0 - 1 - g) % D + D) % D;
+            if (up <= dn) {
+                hi.push_back(g);
+                to_hi = true;
+            } else {
+                lo.push_back(g);
+                to_lo = true;
+            }
+        }
+        // structural symmetry: the rows that read a neighbour are the rows it reads
+        if (to_lo) slo.push_back(i);
+        if (to_hi) shi.push_back(i);
+    }
+    auto uniq = [](std::vector<int64_t>& v) {
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+    };
+    uniq(lo);
+    uniq(hi);
+    p.compact = true;
+    p.halo_lo_rows = std::move(lo);
+    p.halo_hi_rows = std::move(hi);
+    p.halo_lo = static_cast<int64_t>(p.halo_lo_rows.size());
+    p.halo_hi = static_cast<int64_t>(p.halo_hi_rows.size());
+    if (p.halo_lo) p.lo_src_begin = p.halo_lo_rows.front();
+    if (p.halo_hi) p.hi_src_begin = p.halo_hi_rows.front();
+    p.send_lo_rows = std::move(slo);
+    p.send_hi_rows = std::move(shi);
+    return p;
+}
+
+int64_t map_column(const Partition& p, int64_t g) {
+    if (!p.compact) return colmap_of(p).map(g);
+    if (g >= p.row_begin && g < p.row_begin + p.local) return g - p.row_begin + p.halo_lo;
+    auto it = std::lower_bound(p.halo_lo_rows.begin(), p.halo_lo_rows.end(), g);
+    if (it != p.halo_lo_rows.end() && *it == g) return it - p.halo_lo_rows.begin();
+    it = std::lower_bound(p.halo_hi_rows.begin(), p.halo_hi_rows.end(), g);
+    if (it != p.halo_hi_rows.end() && *it == g)
+        return p.halo_lo + p.local + (it - p.halo_hi_rows.begin());
+    return -2;
+}
+
 void plan_sends(Partition& p, int rank, int nranks, const int64_t* all) {
+    if (p.compact) {
+        // what a neighbour reads from us is what we read from it (structural symmetry);
+        // the all-gathered halo sizes must agree with our send lists
+        p.send_lo_n = p.lo_rank >= 0 && nranks > 1 ? static_cast<int64_t>(p.send_lo_rows.size()) : 0;
+        p.send_hi_n = p.hi_rank >= 0 && nranks > 1 ? static_cast<int64_t>(p.send_hi_rows.size()) : 0;
+        if (p.hi_rank >= 0 && nranks > 1 && all[4 * p.hi_rank + 2] == rank &&
+            all[4 * p.hi_rank + 0] != p.send_hi_n)
+            fail(CHEBFD_ERR_UNSUPPORTED, "compact halo: neighbour's request differs (structurally "
+                                         "non-symmetric operator)");
+        if (p.lo_rank >= 0 && nranks > 1 && all[4 * p.lo_rank + 3] == rank &&
+            all[4 * p.lo_rank + 1] != p.send_lo_n)
+            fail(CHEBFD_ERR_UNSUPPORTED, "compact halo: neighbour's request differs (structurally "
+                                         "non-symmetric operator)");
+        return;
+    }
     // my hi neighbour's lo halo is my LAST rows; my lo neighbour's hi halo my FIRST rows
     if (p.hi_rank >= 0 && nranks > 1) {
         const int64_t need = all[4 * p.hi_rank + 0];

@@ -1248,6 +1248,7 @@ void run_step(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
                     grid = static_cast<int>((need + tpc - 1) / tpc);
                     p.tile_a = tpc;
                     launch_kernel = step_tma_kernel<CPLX, T, KIND, DMODE, MW, 1>;
+                    if (nrows > 0) ++ctx.band_launches;
                     if (smem > 48 * 1024)
                         CFD_CUDA(cudaFuncSetAttribute(launch_kernel,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
