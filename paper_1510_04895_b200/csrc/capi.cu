@@ -413,7 +413,15 @@ void run_step_all(Context& c, const Matrix& a, StepArgs s, Block& gathered) {
 // marks its completion: interior rows (no halo reads) concurrently with the exchange,
 // then the boundary rows; the dot partials of the 2-3 launches are reduced by the last.
 void launch_split(Context& c, const Matrix& a, StepArgs s) {
-    const Partition& p = a.part;
+    Partition p = a.part;
+    // lattice operators: widen the boundary regions to whole planes (rows that merely
+    // could run early wait for the halo -- always safe), so every launch covers whole
+    // planes and the band tile order applies to all of them
+    if (a.plane_rows > 0 && p.local % a.plane_rows == 0) {
+        const int64_t P = a.plane_rows;
+        p.bnd_lo = std::min(p.local, (p.bnd_lo + P - 1) / P * P);
+        p.bnd_hi = std::min(p.local - p.bnd_lo, (p.bnd_hi + P - 1) / P * P);
+    }
     int used = 0, base = 0;
     // dot partials of column-slabbed launches cannot be split over interior and boundary
     // launches: such steps wait for the halo and run as one launch per slab
