@@ -106,7 +106,12 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
        CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12, CHEBFD_OPT_PDL = 14,
        CHEBFD_OPT_DELAYED_X = 15, CHEBFD_OPT_BAND_BYTES = 16, CHEBFD_OPT_ASYNC_START = 17,
-       CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19 };
+       CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19, CHEBFD_OPT_GRAM = 20 };
+/* CHEBFD_OPT_GRAM (default 1): gram / SVQB / Rayleigh-Ritz X^H Y of complex blocks of
+ * 48+ columns on the library's own FP64 tensor-core (DMMA) kernel -- split-K over the
+ * rows, only the upper half of Hermitian products (Y^H Y; Q^H A Q of a Hermitian A);
+ * real or narrower blocks on cuBLAS D/ZGEMM.  0 = cuBLAS everywhere, 2 = the DMMA
+ * kernel everywhere (even real widths). */
 /* CHEBFD_OPT_COMPACT_HALO (default 1; set before building distributed matrices): halos of
  * structurally symmetric operators (the lattice models, bitwise-Hermitian from_csr input)
  * hold only the neighbour rows the local rows reference -- TI reads orbitals {0,3} of the

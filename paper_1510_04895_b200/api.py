@@ -178,7 +178,7 @@ class Context:
                 "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
                 "pair_slab": 11, "moments": 12, "pdl": 14, "delayed_x": 15,
                 "band_bytes": 16, "async_start": 17, "tiles_per_cta": 18,
-                "compact_halo": 19}[name]
+                "compact_halo": 19, "gram": 20}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):

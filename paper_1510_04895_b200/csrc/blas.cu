@@ -8,6 +8,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <complex>
 #include <vector>
 
@@ -36,12 +37,21 @@ void destroy_cusolver(Context& c) {
     c.cusolver = nullptr;
 }
 
-void gemm_gram(Context& c, const Block& x, const Block& y, void* dev_out) {
+void gemm_gram(Context& c, const Block& x, const Block& y, void* dev_out, bool herm) {
     const int nx = static_cast<int>(x.width), ny = static_cast<int>(y.width);
     const int64_t rows = x.rows;
     if (nx == 0 || ny == 0) return;
     if (rows == 0) {
         CFD_CUDA(cudaMemsetAsync(dev_out, 0, static_cast<size_t>(nx) * ny * x.scalar_bytes(), c.stream));
+        return;
+    }
+    // the hand-written FP64 tensor-core kernel (gram.cu) for complex blocks of 48+ columns
+    // (measured: at par with cuBLAS on one 64-column super-tile, its Hermitian half pays at
+    // n_b = 256); cuBLAS for real and narrow blocks, where its kernels are faster
+    // (tools/gram_exp.py, profiles/r02_gram_ab.jsonl); CHEBFD_OPT_GRAM = 2 forces it
+    if ((c.gram_mode == 1 && x.kind == CHEBFD_COMPLEX128 && std::min(nx, ny) >= 48) ||
+        (c.gram_mode == 2 && (x.kind == CHEBFD_COMPLEX128 || (nx % 2 == 0 && ny % 2 == 0)))) {
+        gram_dmma(c, x, y, dev_out, herm);
         return;
     }
     require(rows < (1LL << 31), "gram: row count exceeds the cuBLAS 32-bit k dimension");

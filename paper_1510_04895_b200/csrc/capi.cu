@@ -825,13 +825,13 @@ void column_dots_host(Context& c, const Block& x, const Block& y, void* out) {
     ctx_sync(c);
 }
 
-void gram_host(Context& c, const Block& x, const Block& y, void* out) {
+void gram_host(Context& c, const Block& x, const Block& y, void* out, bool herm) {
     if (x.rows != y.rows || x.kind != y.kind)
         fail(CHEBFD_ERR_INVALID_ARGUMENT, "gram: dimension mismatch");
     const int64_t nx = x.width, ny = y.width;
     const size_t bytes = static_cast<size_t>(nx * ny) * x.scalar_bytes();
     c.dscratch.ensure(std::max<size_t>(bytes, 16));
-    gemm_gram(c, x, y, c.dscratch.p);
+    gemm_gram(c, x, y, c.dscratch.p, herm);
     allreduce_sum(c, c.dscratch.as<double>(), bytes / 8, c.stream);
     CFD_CUDA(cudaMemcpyAsync(out, c.dscratch.p, bytes, cudaMemcpyDeviceToHost, c.stream));
     ctx_sync(c);
@@ -1037,6 +1037,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->band_bytes = value;
         else if (option == CHEBFD_OPT_ASYNC_START)
             c->async_start_entries = value;
+        else if (option == CHEBFD_OPT_GRAM)
+            c->gram_mode = static_cast<int>(value);
         else if (option == CHEBFD_OPT_COMPACT_HALO)
             c->compact_halo = value != 0;
         else if (option == CHEBFD_OPT_TILES_PER_CTA)

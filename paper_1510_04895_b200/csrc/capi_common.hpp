@@ -79,13 +79,17 @@ void enqueue_filter(Context& c, const Matrix& a, Block& x, int degree, double al
                     const std::function<void(const StepArgs&, Block&)>& run);
 void allreduce_sum(Context& c, double* dev, size_t n, cudaStream_t st);
 void column_dots_host(Context& c, const Block& x, const Block& y, void* out);
-void gram_host(Context& c, const Block& x, const Block& y, void* out);
+void gram_host(Context& c, const Block& x, const Block& y, void* out, bool herm = false);
 void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* combined, int degree,
                          double alpha, double beta, double* moments_host);
 
 // blas.cu: cuBLAS / cuSOLVER wrappers on row-major blocks
 // dev_out (row-major nx x ny, local rows only) = X^H Y
-void gemm_gram(Context& c, const Block& x, const Block& y, void* dev_out);
+// herm: the product is known Hermitian (Rayleigh-Ritz Q^H A Q) -- only its upper half
+// need be computed
+void gemm_gram(Context& c, const Block& x, const Block& y, void* dev_out, bool herm = false);
+// the same on the FP64 tensor cores, hand-written (gram.cu)
+void gram_dmma(Context& c, const Block& x, const Block& y, void* dev_out, bool herm);
 // Y = X B with B given on the host (row-major nb x bcols)
 void mult_small_host_b(Context& c, const Block& x, const void* b_host, int64_t bcols, Block& y);
 // Y = X B with B on the device (row-major)

@@ -238,6 +238,8 @@ struct Context {
     DeviceBuffer workspace;  // cuSOLVER / misc
     DeviceBuffer devinfo;
     DeviceBuffer coeffs;     // filter coefficients (device copy)
+    DeviceBuffer gram_scratch;  // DMMA Gram: super-tile list + split-K partial tiles
+    int gram_mode = 1;       // X^H Y: 1 hand-written DMMA kernel (gram.cu), 0 cuBLAS; CHEBFD_OPT_GRAM
     DeviceBuffer small[4];   // host-fed small operands (rotations, eigenvalues, Gram, eig)
     // exact-size cache of block storage: the solver allocates the same blocks every
     // iteration, and cudaFree synchronises the device.  All work on a block is

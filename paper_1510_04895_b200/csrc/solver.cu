@@ -104,7 +104,9 @@ Ritz rayleigh_ritz(Context& c, const Matrix& a, Block& q) {
     s.beta = 0.0;
     run_step_all(c, a, s, q);
     Small p(q.kind, nb, nb);
-    gram_host(c, q, *aq, p.a.data());
+    // P = Q^H (A Q) is Hermitian (A Hermitian): its upper half suffices; symmetrize keeps
+    // the reference's P = (G + G^H) / 2 (solver.cpp:68-70) for non-Hermitian input
+    gram_host(c, q, *aq, p.a.data(), a.hermitian);
     symmetrize(p);
     Ritz out;
     out.values.resize(nb);
