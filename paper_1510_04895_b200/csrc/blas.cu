@@ -81,6 +81,11 @@ void mult_small_dev_b(Context& c, const Block& x, const void* b_dev, int64_t bco
         CFD_CUDA(cudaMemsetAsync(y.owned(), 0, y.owned_bytes(), c.stream));
         return;
     }
+    // complex rotations of 48+ columns on the hand-written DMMA kernel (gram.cu), as the Gram
+    if (x.kind == CHEBFD_COMPLEX128 && c.gram_mode >= 1 && (std::min(nb, m) >= 48 || c.gram_mode == 2)) {
+        tsgemm_dmma(c, x, b_dev, bcols, y);
+        return;
+    }
     require(rows < (1LL << 31), "block_mult_small: row count exceeds 32-bit n dimension");
     if (x.kind == CHEBFD_REAL64) {
         const double one = 1.0, zero = 0.0;

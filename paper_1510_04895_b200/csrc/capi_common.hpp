@@ -90,6 +90,8 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
 void gemm_gram(Context& c, const Block& x, const Block& y, void* dev_out, bool herm = false);
 // the same on the FP64 tensor cores, hand-written (gram.cu)
 void gram_dmma(Context& c, const Block& x, const Block& y, void* dev_out, bool herm);
+// Y = X B (complex, B row-major nb x bcols on the device) on the FP64 tensor cores (gram.cu)
+void tsgemm_dmma(Context& c, const Block& x, const void* b_dev, int64_t bcols, Block& y);
 // Y = X B with B given on the host (row-major nb x bcols)
 void mult_small_host_b(Context& c, const Block& x, const void* b_host, int64_t bcols, Block& y);
 // Y = X B with B on the device (row-major)

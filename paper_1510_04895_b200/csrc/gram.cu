@@ -1,4 +1,5 @@
-// Tall-skinny Gram G = X^H Y on FP64 tensor cores (DMMA), hand-written for sm_100a.
+// Tall-skinny Gram G = X^H Y and block rotation Y = X B on FP64 tensor cores (DMMA),
+// hand-written for sm_100a.
 //
 // gram (kernels.hpp:165-192) is G(k,l) = <x_k, y_l> over D rows of two row-major blocks
 // of widths nx, ny <= a few hundred: a GEMM with a huge K (D up to 67 M) and a small
@@ -213,7 +214,136 @@ __global__ void gram_reduce_kernel(const double2* __restrict__ partials, const i
     }
 }
 
+// ---- block_mult_small Y = X B (kernels.hpp:216-232) on the FP64 tensor cores ------------
+// M = this rank's rows, N = m (B's columns), K = n_b.  CTA tile 64 rows x 64 columns of
+// Y, K streamed in 16-wide chunks of X (row-major, pitch 17 complex: the 8 rows x 4 k of
+// a fragment fill distinct bank groups) and of B (row-major, L2-resident across tiles);
+// the same warp layout and fragments as the Gram: Re += Xr Br - Xi Bi, Im += Xr Bi + Xi Br.
+struct TsParams {
+    const double2* x;   // rows x nb
+    const double2* b;   // nb x m, row-major
+    double2* y;         // rows x m
+    int64_t rows;
+    int nb, m;
+};
+
+constexpr int kXP = kKS + 1;  // X tile row pitch (complex): fragment rows fall in distinct banks
+constexpr int kTsStage = kTS * kXP + kKS * kTS;  // complex entries per stage (X tile + B chunk)
+
+__global__ void __launch_bounds__(kThreads, 2) tsgemm_dmma_kernel(const TsParams p) {
+    extern __shared__ __align__(16) unsigned char tsm_raw[];
+    double2* sm = reinterpret_cast<double2*>(tsm_raw);
+    // stage st: X tile [64 rows][kXP] row-major (as in global), B chunk [kKS][64]
+    auto xs = [&](int st) { return sm + st * kTsStage; };
+    auto bs = [&](int st) { return sm + st * kTsStage + kTS * kXP; };
+    const int64_t R0 = static_cast<int64_t>(blockIdx.x) * kTS;
+    const int N0 = blockIdx.y * kTS;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    auto issue = [&](int st, int K0) {
+        for (int q = t; q < kKS * kTS; q += kThreads) {
+            // X: row i, k-column kk of the chunk -> xs[i][kk] (coalesced along k)
+            const int i = q / kKS, kk = q - i * kKS;
+            const int64_t r = R0 + i;
+            const bool xin = r < p.rows && K0 + kk < p.nb;
+            cp_async16(xs(st) + i * kXP + kk, p.x + (xin ? r * p.nb + K0 + kk : 0), xin);
+            // B: k-row bk, column n -> bs[bk][n]
+            const int bk = q / kTS, n = q - bk * kTS;
+            const bool bin = K0 + bk < p.nb && N0 + n < p.m;
+            cp_async16(bs(st) + bk * kTS + n, p.b + (bin ? static_cast<int64_t>(K0 + bk) * p.m + N0 + n : 0),
+                       bin);
+        }
+    };
+    const int m0 = 16 * (w >> 1), n0 = 32 * (w & 1);
+    double cre[2][4][2], cim[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            cre[a][b][0] = cre[a][b][1] = 0.0;
+            cim[a][b][0] = cim[a][b][1] = 0.0;
+        }
+    const int fk = lane & 3, fm = lane >> 2;
+    const int nst = (p.nb + kKS - 1) / kKS;
+#pragma unroll
+    for (int s = 0; s < kNST - 1; ++s) {
+        if (s < nst) issue(s, s * kKS);
+        cp_async_commit();
+    }
+    for (int it = 0; it < nst; ++it) {
+        cp_async_wait<kNST - 2>();
+        __syncthreads();
+        if (it + kNST - 1 < nst) issue((it + kNST - 1) % kNST, (it + kNST - 1) * kKS);
+        cp_async_commit();
+        const double2* xa = xs(it % kNST);
+        const double2* bb = bs(it % kNST);
+#pragma unroll
+        for (int ks = 0; ks < kKS; ks += 4) {
+            const int row = (ks + fk) * kTS;
+            double ar[2], ai[2], br[4], bi[4];
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const double2 v = xa[(m0 + 8 * a + fm) * kXP + ks + fk];
+                ar[a] = v.x;
+                ai[a] = v.y;
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double2 v = bb[row + n0 + 8 * b + fm];
+                br[b] = v.x;
+                bi[b] = v.y;
+            }
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(cre[a][b], ar[a], br[b]);
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(cim[a][b], ar[a], bi[b]);
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(cre[a][b], -ai[a], bi[b]);
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(cim[a][b], ai[a], br[b]);
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t r = R0 + m0 + 8 * a + fm;
+                const int n = N0 + n0 + 8 * b + 2 * fk + e;
+                if (r < p.rows && n < p.m) p.y[r * p.m + n] = make_double2(cre[a][b][e], cim[a][b][e]);
+            }
+}
+
 }  // namespace
+
+// Y = X B (complex blocks, B on the device, row-major nb x m) on the FP64 tensor cores.
+void tsgemm_dmma(Context& c, const Block& x, const void* b_dev, int64_t bcols, Block& y) {
+    const int nb = static_cast<int>(x.width), m = static_cast<int>(bcols);
+    require(x.kind == CHEBFD_COMPLEX128, "tsgemm_dmma: complex blocks only");
+    if (x.rows == 0 || m == 0) return;
+    TsParams p{static_cast<const double2*>(x.owned()), static_cast<const double2*>(b_dev),
+               static_cast<double2*>(y.owned()), x.rows, nb, m};
+    const size_t smem = static_cast<size_t>(kNST) * kTsStage * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+        CFD_CUDA(cudaFuncSetAttribute(tsgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        attr = true;
+    }
+    const dim3 grid(static_cast<unsigned>((x.rows + kTS - 1) / kTS), static_cast<unsigned>((m + kTS - 1) / kTS));
+    tsgemm_dmma_kernel<<<grid, kThreads, smem, c.stream>>>(p);
+    CFD_CUDA(cudaGetLastError());
+    c.launches++;
+}
 
 // dev_out (row-major nx x ny, this rank's rows) = X^H Y on the FP64 tensor cores.
 void gram_dmma(Context& c, const Block& x, const Block& y, void* dev_out, bool herm) {

@@ -62,5 +62,45 @@ def main():
     ctx.close()
 
 
+
+
+def tsgemm(reps=3):
+    """block_mult_small Y = X B: the DMMA kernel (gram.cu) against cuBLAS ZGEMM."""
+    ctx = cf.Context(0)
+    for name, l, nb in (("C4 share Y=XB", (512, 512, 8), 64), ("C3 Y=XB", (128, 128, 64), 256),
+                        ("C2 Y=XB", (64, 64, 64), 32)):
+        A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(*l, disorder=0.5, seed=1))
+        X = cf.BlockVector(A, nb).randomize_device(1)
+        rng = np.random.default_rng(3)
+        B = (rng.standard_normal((nb, nb)) + 1j * rng.standard_normal((nb, nb))).astype(np.complex128)
+        out, res = {}, {}
+        for mode in (0, 2):
+            ctx.set_option("gram", mode)
+            Y = cf.block_mult_small(X, B)
+            res[mode] = Y.to_numpy()[:4096]
+            Y.close()
+            ctx.synchronize()
+            ctx.record(0)
+            for _ in range(reps):
+                Y = cf.block_mult_small(X, B)
+                Y.close()
+            ctx.record(1)
+            out[mode] = ctx.elapsed_ms(0, 1) / reps
+        flops = 8 * A.dim() * nb * nb
+        print(json.dumps({"case": name, "D": A.dim(), "nb": nb, "cublas_ms": round(out[0], 3),
+                          "dmma_ms": round(out[2], 3), "cublas_tflops": round(flops / out[0] * 1e-9, 2),
+                          "dmma_tflops": round(flops / out[2] * 1e-9, 2),
+                          "speedup": round(out[0] / out[2], 3),
+                          "rel_diff": float(np.max(np.abs(res[2] - res[0])) / np.max(np.abs(res[0])))}),
+              flush=True)
+        X.close()
+        A.close()
+    ctx.set_option("gram", 1)
+    ctx.close()
+
+
 if __name__ == "__main__":
-    main()
+    if "--tsgemm" in sys.argv:
+        tsgemm()
+    else:
+        main()
