@@ -365,7 +365,8 @@ def run_e2e(cf, ctx, A, p, nb, Dl, do_gram, flops_step, args, dist, rank):
     rng = np.random.default_rng(rank)
     xa.view(np.float64)[:] = rng.standard_normal((Dl, 2 * nb))
     xb[:] = xa
-    gram_h = [np.zeros((nb, nb), np.complex128) for _ in range(2)]
+    # pinned: a device -> pageable host copy would block the host until the filter ends
+    gram_h = [cf.host_array((nb, nb), np.complex128) for _ in range(2)]
     bufs = (xa, xb)
     pipe = cf.FilterPipe(A, nb)
 
@@ -524,7 +525,7 @@ def main():
     ap.add_argument("--degree", type=int, default=0, help="N_p (0: the workload's)")
     ap.add_argument("--strong", action="store_true",
                     help="N >= 2: also the full 512x512x64 lattice split over the ranks")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -724,7 +724,9 @@ class FilterPipe:
     def submit(self, x_in: np.ndarray, p: "FilterPolynomial", x_out: Optional[np.ndarray] = None,
                gram_out: Optional[np.ndarray] = None):
         """Queue one filter of x_in (result in x_out, default in place); with gram_out
-        (width x width, matrix dtype) also the Gram X^H X of the filtered block."""
+        (width x width, matrix dtype) also the Gram X^H X of the filtered block.  Pass
+        pinned arrays (host_array): copies to or from pageable memory block the host until
+        the stream reaches them, which serialises the pipeline."""
         x_out = x_in if x_out is None else x_out
         for x in (x_in, x_out):
             if x.dtype != self.A.dtype or not x.flags.c_contiguous or x.shape != (self.A.local_rows, self.width_):

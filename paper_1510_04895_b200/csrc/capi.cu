@@ -766,6 +766,7 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
             if (moments) e.moments = std::make_shared<DeviceBuffer>(mom_alloc);
             CFD_CUDA(cudaMemcpyAsync(e.coeff->p, combined, coeff_bytes, cudaMemcpyHostToDevice,
                                      c.stream));
+            e.coeff_host.assign(combined, combined + degree + 1);
             ctx_sync(c);
             cudaGraph_t g;
             const int64_t before = c.launches;
@@ -784,9 +785,10 @@ void apply_filter_device(Context& c, const Matrix& a, Block& x, const double* co
             CFD_CUDA(cudaGraphInstantiate(&e.exec, g, 0));
             CFD_CUDA(cudaGraphDestroy(g));
             it = c.graphs.emplace(key, e).first;
-        } else {
+        } else if (!std::equal(combined, combined + degree + 1, it->second.coeff_host.begin())) {
             CFD_CUDA(cudaMemcpyAsync(it->second.coeff->p, combined, coeff_bytes,
                                      cudaMemcpyHostToDevice, c.stream));
+            it->second.coeff_host.assign(combined, combined + degree + 1);
         }
         CFD_CUDA(cudaGraphLaunch(it->second.exec, c.stream));
         c.launches += it->second.kernels;

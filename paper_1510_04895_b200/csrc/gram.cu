@@ -364,14 +364,16 @@ void gram_dmma(Context& c, const Block& x, const Block& y, void* dev_out, bool h
     const int64_t rows = x.rows;
     int S = std::max(1, (2 * c.num_sms + T - 1) / T);
     S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(S, (rows + kKS - 1) / kKS)));
-    // scratch: tile list + partials (sized before any graph capture by the caller's
-    // first use; gram is not captured)
-    const size_t tbytes = sizeof(int2) * T;
+    // the super-tile list, uploaded once per shape; the partials scratch grows only
+    auto& tb = c.gram_tiles[std::make_tuple(nx, ny, same)];
+    if (!tb) {
+        tb = std::make_unique<DeviceBuffer>(sizeof(int2) * T);
+        CFD_CUDA(cudaMemcpy(tb->p, tl.data(), sizeof(int2) * T, cudaMemcpyHostToDevice));
+    }
+    int2* d_tiles = tb->as<int2>();
     const size_t pbytes = sizeof(double2) * static_cast<size_t>(S) * T * kTS * kTS;
-    c.gram_scratch.ensure(tbytes + pbytes + 256);
-    int2* d_tiles = c.gram_scratch.as<int2>();
-    double2* d_part = reinterpret_cast<double2*>(c.gram_scratch.as<char>() + ((tbytes + 255) & ~size_t(255)));
-    CFD_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), tbytes, cudaMemcpyHostToDevice, c.stream));
+    c.gram_scratch.ensure(pbytes);
+    double2* d_part = c.gram_scratch.as<double2>();
     GramParams p{x.owned(), y.owned(), rows, nx, ny, d_tiles, S, d_part, one_slab ? 1 : 0};
     const size_t smem = static_cast<size_t>(kNST) * 2 /*operands*/ * kKS *
                         (cplx ? pitch_of<true>() * sizeof(double2) : pitch_of<false>() * sizeof(double));

@@ -183,6 +183,10 @@ struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     std::shared_ptr<DeviceBuffer> coeff, moments;
     int64_t kernels = 0;
+    // the coefficients now in `coeff`: a replay with the same filter skips the host ->
+    // device copy (a pageable copy would first wait for the stream to drain, which
+    // serialises streamed submissions behind the previous filter)
+    std::vector<double> coeff_host;
 };
 
 struct FilterWorkspace {
@@ -238,7 +242,10 @@ struct Context {
     DeviceBuffer workspace;  // cuSOLVER / misc
     DeviceBuffer devinfo;
     DeviceBuffer coeffs;     // filter coefficients (device copy)
-    DeviceBuffer gram_scratch;  // DMMA Gram: super-tile list + split-K partial tiles
+    DeviceBuffer gram_scratch;  // DMMA Gram: split-K partial tiles
+    // DMMA Gram super-tile lists per (nx, ny, Hermitian) (uploaded once: no per-call
+    // pageable copy, which would wait for the stream to drain)
+    std::map<std::tuple<int, int, bool>, std::unique_ptr<DeviceBuffer>> gram_tiles;
     int gram_mode = 1;       // X^H Y: 1 hand-written DMMA kernel (gram.cu), 0 cuBLAS; CHEBFD_OPT_GRAM
     DeviceBuffer small[4];   // host-fed small operands (rotations, eigenvalues, Gram, eig)
     // exact-size cache of block storage: the solver allocates the same blocks every
