@@ -199,6 +199,7 @@ AsyncRandomize::AsyncRandomize(Context& c, Block& b, uint64_t seed) {
             char* dev = static_cast<char*>(b.owned());
             const int64_t piece = std::min(kPiece, std::max<int64_t>(count, 1));
             for (int64_t off = 0, k = 0; off < count; off += piece, ++k) {
+                if (cancel_.load(std::memory_order_relaxed)) break;  // block no longer wanted
                 const int buf = static_cast<int>(k & 1);
                 const int64_t n = std::min(piece, count - off);
                 char* h = pin + buf * piece * esz;
@@ -229,6 +230,9 @@ void AsyncRandomize::join() {
 }
 
 AsyncRandomize::~AsyncRandomize() {
+    // not joined (an early return or an error before the block was needed): stop after the
+    // piece in flight instead of generating the rest
+    cancel_.store(true, std::memory_order_relaxed);
     if (th_.joinable()) th_.join();
 }
 

@@ -1,5 +1,6 @@
 // Helpers shared by the C-ABI translation units (capi.cu, solver.cu, blas.cu).
 #pragma once
+#include <atomic>
 #include <exception>
 #include <functional>
 #include <thread>
@@ -52,6 +53,7 @@ class AsyncRandomize {
   private:
     std::thread th_;
     std::exception_ptr err_;
+    std::atomic<bool> cancel_{false};
 };
 void check_conforms(const Matrix& a, const Block& x, const char* who);
 // moments by the Chebyshev doubling identities (CHEBFD_OPT_MOMENTS, Hermitian operators)

@@ -232,3 +232,31 @@ def test_solve_automatic_degree_matches_reference(ctx):
     acc = np.sort(rep.ritz.values[rep.ritz.accepted])
     assert np.max(np.abs(acc - np.array(g["accepted_values"]))) <= 1e-10
     assert set(rep.timings) == {"bounds", "dos", "design", "filter", "ortho", "rr", "start"}
+
+
+def test_async_start_block_equals_synchronous(ctx):
+    """With N_S given, solve() generates the start block on a helper thread while the
+    device runs the bounds and the KPM DOS (CHEBFD_OPT_ASYNC_START, default above 2^26
+    entries).  Lowered to every size, it must give the synchronous path's bits: the same
+    Ritz values, residuals and iteration count."""
+    A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(6, 6, 6, disorder=0.5, seed=4))
+    opts = cf.SolverOptions(target=cf.Interval(-0.45, 0.45), n_search=16, degree=60, seed=3,
+                            dos_moments=300, dos_samples=8)
+    ctx.set_option("async_start", 0)
+    try:
+        sync = cf.solve(A, opts)
+        ctx.set_option("async_start", 1)  # every start block on the helper thread
+        asyn = cf.solve(A, opts)
+    finally:
+        ctx.set_option("async_start", 1 << 26)
+    assert asyn.iterations == sync.iterations and asyn.converged == sync.converged
+    assert np.array_equal(asyn.ritz.values, sync.ritz.values)
+    assert np.array_equal(asyn.ritz.residual_norms, sync.ritz.residual_norms)
+    # the empty-target early return joins the helper cleanly
+    ctx.set_option("async_start", 1)
+    try:
+        rep = cf.solve(A, cf.SolverOptions(target=cf.Interval(9.0, 9.5), n_search=16, degree=60,
+                                           bounds=cf.Interval(-10.0, 10.0)))
+        assert rep.converged and rep.iterations == 0
+    finally:
+        ctx.set_option("async_start", 1 << 26)
