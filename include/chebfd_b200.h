@@ -106,7 +106,17 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_PAIR_THREADS = 8, CHEBFD_OPT_PAIR_EXTRA = 9, CHEBFD_OPT_PAIR_HINTS = 10,
        CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12, CHEBFD_OPT_PDL = 14,
        CHEBFD_OPT_DELAYED_X = 15, CHEBFD_OPT_BAND_BYTES = 16, CHEBFD_OPT_ASYNC_START = 17,
-       CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19, CHEBFD_OPT_GRAM = 20 };
+       CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19, CHEBFD_OPT_GRAM = 20,
+       CHEBFD_OPT_GROUPED = 21, CHEBFD_OPT_GROUP_LINES = 22 };
+/* CHEBFD_OPT_GROUPED (default 1): dot-free steps that run in the band tile order (lattice
+ * operators whose z-planes exceed the L2 budget, CHEBFD_OPT_BAND_BYTES) use the row-group
+ * kernel: four consecutive rows -- a lattice site's orbitals -- share one merged list of
+ * gathered rows, sites of the TI stencil run straight-line code with two multiplies per
+ * purely real / imaginary matrix entry.  W and X are bit-identical to the SELL kernels for
+ * finite inputs (see csrc/group_patterns.hpp for the sign of exact zeros).  2: every step
+ * on every operator with a grouped form (tests); 0: the SELL kernels only.
+ * CHEBFD_OPT_GROUP_LINES (default 1; set before building matrices): tiles of the grouped
+ * form span 1, 2 or 4 lattice lines (measured: no gain from 2 or 4). */
 /* CHEBFD_OPT_GRAM (default 1): gram / SVQB / Rayleigh-Ritz X^H Y of complex blocks of
  * 48+ columns on the library's own FP64 tensor-core (DMMA) kernel -- split-K over the
  * rows, only the upper half of Hermitian products (Y^H Y; Q^H A Q of a Hermitian A);
@@ -148,6 +158,8 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
  * the steps reduce (KPM: half the recurrence steps).  Equal up to rounding. */
 /* step launches that ran in the band tile order (CHEBFD_OPT_BAND_BYTES) so far */
 int chebfd_ctx_band_launches(chebfd_ctx* ctx, int64_t* count);
+/* step launches that ran the row-group kernel (CHEBFD_OPT_GROUPED) so far */
+int chebfd_ctx_group_launches(chebfd_ctx* ctx, int64_t* count);
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */

@@ -153,6 +153,13 @@ class Context:
         return v.value
 
     @property
+    def group_launches(self) -> int:
+        """Step launches that ran the row-group kernel (option "grouped")."""
+        v = C.c_int64()
+        _check(_lib().chebfd_ctx_group_launches(self._h, C.byref(v)))
+        return v.value
+
+    @property
     def band_launches(self) -> int:
         """Step launches that ran in the band (2.5D) tile order."""
         v = C.c_int64()
@@ -178,7 +185,7 @@ class Context:
                 "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
                 "pair_slab": 11, "moments": 12, "pdl": 14, "delayed_x": 15,
                 "band_bytes": 16, "async_start": 17, "tiles_per_cta": 18,
-                "compact_halo": 19, "gram": 20}[name]
+                "compact_halo": 19, "gram": 20, "grouped": 21, "group_lines": 22}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -507,9 +508,12 @@ void setup_partition(Context& c, Matrix& m, const HostCsr& csr, int64_t r0, int6
 
 std::unique_ptr<Matrix> matrix_from_host_csr(Context& c, const HostCsr& csr, int64_t r0, int64_t r1,
                                              const std::vector<int64_t>& starts, int64_t nnz_global,
-                                             bool symmetric) {
+                                             bool symmetric, int64_t plane_rows = 0,
+                                             int64_t line_rows = 0) {
     auto m = std::make_unique<Matrix>();
     m->ctx = &c;
+    m->plane_rows = plane_rows;  // known before the build: the grouped form tiles by lines
+    m->line_rows = line_rows;
     m->kind = csr.kind;
     m->nnz_local = static_cast<int64_t>(csr.cols.size());
     m->nnz_global = nnz_global;
@@ -578,12 +582,10 @@ std::unique_ptr<Matrix> lattice_matrix(Context& c, const chebfd_lattice& s, bool
     const int64_t nnz_g = allreduce_count(c, static_cast<int64_t>(csr.cols.size()));
     // both models add every hopping with its conjugate (models.cpp:80-178): Hermitian,
     // hence structurally symmetric (compact halos apply)
-    auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g, true);
+    // TI: row = 4 (x + Lx (y + Ly z)) + orbital (models.hpp:15-19)
+    auto m = matrix_from_host_csr(c, csr, r0, r1, starts, nnz_g, true, ti ? 4 * s.lx * s.ly : 0,
+                                  ti ? 4 * s.lx : 0);
     m->hermitian = true;
-    if (ti) {  // row = 4 (x + Lx (y + Ly z)) + orbital (models.hpp:15-19)
-        m->plane_rows = 4 * s.lx * s.ly;
-        m->line_rows = 4 * s.lx;
-    }
     return m;
 }
 
@@ -905,6 +907,9 @@ static void ctx_init(Context& c, int device) {
     c.counter.ensure(4096);  // grid ticket + group tickets of grid_reduce
     CFD_CUDA(cudaMemsetAsync(c.counter.p, 0, 4096, c.stream));
     c.dscratch.ensure(1 << 20);
+    // test hook: CHEBFD_GROUPED=2 runs the whole suite on the row-group kernel
+    if (const char* e = std::getenv("CHEBFD_GROUPED")) c.grouped = std::atoi(e);
+    if (const char* e = std::getenv("CHEBFD_GROUP_LINES")) c.group_lines = std::atoi(e);
     ctx_sync(c);
 }
 
@@ -1006,6 +1011,10 @@ int chebfd_ctx_launch_count(chebfd_ctx* ctx, int64_t* count) {
     return guard([&] { *count = reinterpret_cast<Context*>(ctx)->launches; });
 }
 
+int chebfd_ctx_group_launches(chebfd_ctx* ctx, int64_t* count) {
+    return guard([&] { *count = reinterpret_cast<Context*>(ctx)->group_launches; });
+}
+
 int chebfd_ctx_band_launches(chebfd_ctx* ctx, int64_t* count) {
     return guard([&] { *count = reinterpret_cast<Context*>(ctx)->band_launches; });
 }
@@ -1047,6 +1056,10 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->gram_mode = static_cast<int>(value);
         else if (option == CHEBFD_OPT_COMPACT_HALO)
             c->compact_halo = value != 0;
+        else if (option == CHEBFD_OPT_GROUPED)
+            c->grouped = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_GROUP_LINES)
+            c->group_lines = static_cast<int>(value);
         else if (option == CHEBFD_OPT_TILES_PER_CTA)
             c->tiles_per_cta = static_cast<int>(std::max<int64_t>(value, 0));
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)

@@ -106,6 +106,40 @@ constexpr int kChunk = 32;
 constexpr int kStageRuns = 64;  // row runs per chunk in a staged-gather plan
 constexpr int kStageGap = 3;    // runs closer than this many rows are merged (copied together)
 
+// ---- grouped matrix: row groups of 4 with merged (union) column lists ---------------
+// Rows 4g .. 4g+3 share one list of gathered columns: entry k = extended-row index
+// (low 28 bits) | row mask (high 4 bits); for every set bit r, in increasing r, the next
+// value of the group multiplies in[col] into row r's sum.  Each row meets its entries in
+// its CSR order (the merge keeps every row's order), so the sums are bit-identical to the
+// SELL kernels; a lattice site's 4 orbitals share their 24 neighbour rows instead of
+// gathering 44 (TI), which halves the L1 traffic of a step.
+// Tiles of kTileGroups groups (64 rows) are contiguous: cols = [int4 header per group:
+// (column offset in the tile's segment, value offset, padded column count, column count)]
+// + the groups' packed columns (padded to multiples of 4 with mask-0 copies);
+// vals = the groups' values in processing order.
+constexpr int kGroupRows = 4;
+constexpr int kTileGroups = 16;
+constexpr int kTileRows = kGroupRows * kTileGroups;
+constexpr int kGroupMaxRowLen = 32;  // longer rows: no grouped form
+struct GroupedMatrix {
+    bool ok = false;
+    int64_t ntiles = 0;
+    DeviceBuffer tile_cptr;  // int64[ntiles+1]: first int of tile t in cols
+    DeviceBuffer tile_vptr;  // int64[ntiles+1]: first value of tile t in vals
+    DeviceBuffer cols;       // int32
+    DeviceBuffer vals;       // double / double2
+    int64_t ncols = 0, nvals = 0;
+    int max_tile_cols = 0, max_tile_vals = 0;  // per-tile maxima (shared-memory stage size)
+    // Lattice operators: a tile is a patch of il_lines lattice lines x (16 / il_lines)
+    // sites instead of 16 consecutive sites, so the y -+ 1 neighbour rows of its groups are
+    // each other's own rows and reach the L1 once (il_line_rows rows per line; 0: linear
+    // tiles).  Tile t still covers rows inside [64 t', 64 t' + 64)'s line group, so every
+    // launch range of whole line groups is the same set of tiles in both numberings.
+    int64_t il_line_rows = 0;
+    int il_lines = 1;
+    std::vector<std::pair<double, std::unique_ptr<DeviceBuffer>>> scaled;
+};
+
 struct Matrix {
     Context* ctx = nullptr;
     int kind = 0;
@@ -141,6 +175,7 @@ struct Matrix {
     // buffers they are gathered into before ncclSend, and -- virtual groups -- the
     // neighbours' local indices of this rank's halo rows (pulled by a gather kernel)
     DeviceBuffer send_lo_idx, send_hi_idx, pack_lo, pack_hi, recv_lo_src, recv_hi_src;
+    GroupedMatrix grp;  // grouped form (default step kernel where it applies)
 };
 
 // ---- block vector -------------------------------------------------------------------
@@ -234,6 +269,12 @@ struct Context {
     // step launches without dots: non-persistent grids of this many consecutive row tiles
     // per CTA (0: persistent CTA-strided grids everywhere); CHEBFD_OPT_TILES_PER_CTA
     int tiles_per_cta = 2;
+    // row-group step kernel (step_group.cuh) where the grouped form applies;
+    // CHEBFD_OPT_GROUPED (0: SELL kernels only)
+    int grouped = 1;
+    int group_lines = 1;  // lattice lines per tile of the grouped form (1: linear); set before
+                          // building matrices (CHEBFD_OPT_GROUP_LINES)
+    int64_t group_launches = 0;  // step launches that ran the row-group kernel
     // exchange only the referenced halo rows of structurally symmetric operators (lattice
     // models, bitwise-Hermitian from_csr input); CHEBFD_OPT_COMPACT_HALO
     bool compact_halo = true;
@@ -303,6 +344,31 @@ void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st);
 void launch_step_c(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
 void launch_step_r2(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
 void launch_step_r1(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
+// row-group step kernel (step_gc.cu / step_gr2.cu / step_gr1.cu): false = does not apply
+// to this launch (nothing launched)
+bool launch_group_c(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
+bool launch_group_r2(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
+bool launch_group_r1(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
+// group gi of tile t of a grouped matrix -> its first row (linear or line-interleaved tiles)
+struct TileMap {
+    int64_t line_rows;  // 0: linear
+    int lines;          // lattice lines per tile
+    int64_t tpl;        // tiles per line group (x blocks)
+    CFD_HD int64_t first_row(int64_t t, int gi) const {
+        if (line_rows == 0) return t * kTileRows + gi * kGroupRows;
+        const int64_t lg = t / tpl, xb = t - lg * tpl;
+        const int xs = kTileGroups / lines;  // sites per tile line
+        const int xi = gi / lines, yi = gi - xi * lines;
+        return lg * lines * line_rows + yi * line_rows + (xb * xs + xi) * kGroupRows;
+    }
+};
+inline TileMap tilemap_of(const GroupedMatrix& g) {
+    return TileMap{g.il_line_rows, g.il_lines,
+                   g.il_line_rows ? g.il_line_rows / (kGroupRows * (kTileGroups / g.il_lines)) : 1};
+}
+// grouped form of a device CSR (group.cu); leaves m.grp.ok = false where it does not apply
+void build_grouped(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d_cols,
+                   const void* d_vals, cudaStream_t st);
 // column-slab launches launch_step will use for s (an upper bound: >= the real count)
 int step_slab_count(const Context& ctx, const StepArgs& s);
 // Steps coeff_index and coeff_index+1 of apply_filter's fused loop in one

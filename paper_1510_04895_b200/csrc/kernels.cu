@@ -339,15 +339,23 @@ int step_slab_count(const Context& ctx, const StepArgs& s) {
 void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st) {
     const int kind = s.a->kind;
     const int64_t width = s.width_cols;
-    if (kind == CHEBFD_COMPLEX128)
-        launch_step_c(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
-    else if (width % 2 == 0)
-        launch_step_r2(ctx, s, st, static_cast<int>(width / 2), static_cast<int>(width / 2));
-    else
-        launch_step_r1(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
+    // the row-group kernel where the grouped form applies, else the SELL kernels
+    if (kind == CHEBFD_COMPLEX128) {
+        if (!launch_group_c(ctx, s, st, static_cast<int>(width), static_cast<int>(width)))
+            launch_step_c(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
+    } else if (width % 2 == 0) {
+        if (!launch_group_r2(ctx, s, st, static_cast<int>(width / 2), static_cast<int>(width / 2)))
+            launch_step_r2(ctx, s, st, static_cast<int>(width / 2), static_cast<int>(width / 2));
+    } else {
+        if (!launch_group_r1(ctx, s, st, static_cast<int>(width), static_cast<int>(width)))
+            launch_step_r1(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
+    }
 }
 
+void ensure_scaled_grouped(Context& ctx, Matrix& a, double s, cudaStream_t st);  // group.cu
+
 void ensure_scaled_values(Context& ctx, Matrix& a, double s, cudaStream_t st) {
+    ensure_scaled_grouped(ctx, a, s, st);
     if (find_scaled(a, s)) return;
     if (a.scaled.size() >= 4) {
         // graphs may reference the evicted copy: the caller purges them
@@ -540,6 +548,7 @@ void build_sell(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d
     CFD_CUDA(cudaStreamSynchronize(st));
     if (err) fail(CHEBFD_ERR_UNSUPPORTED, "matrix column outside this rank's rows and halos");
     m.band = static_cast<int64_t>(band);
+    build_grouped(ctx, m, d_offs, d_cols, d_vals, st);
     // pair kernel tickets + one completion counter per 1024-row group, zeroed once
     // (every launch leaves them zeroed)
     const size_t groups = static_cast<size_t>((m.nchunks + 31) / 32);

@@ -286,12 +286,12 @@ int chebfd_vgroup_matrix_lattice(chebfd_vgroup* g, int model, const chebfd_latti
             Context& c = *v.ranks[r];
             Matrix& mr = *m[r];
             mr.nnz_global = nnz;
-            build_matrix_device(c, mr, csr[r]);
-            mr.hermitian = true;
             if (ti) {
                 mr.plane_rows = 4 * spec->lx * spec->ly;
                 mr.line_rows = 4 * spec->lx;
             }
+            build_matrix_device(c, mr, csr[r]);
+            mr.hermitian = true;
             // the neighbours' local indices of this rank's halo rows (pulled by rank r)
             const Partition& p = mr.part;
             auto src_list = [&](int q, bool lo) {
