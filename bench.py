@@ -58,7 +58,7 @@ WORKLOADS = {
     "c2": (64, 64, 64, 32, 100, False, "configs[1]"),
 }
 NCU_TRAFFIC = {  # committed ncu captures of the dominant kernel for a workload
-    "c4": "profiles/r02_c4_recur_step.json",
+    "c4": "profiles/r02b_c4_recur_step.json",
     "c2": "profiles/r02_c2_recur_step.json",
 }
 
@@ -267,10 +267,12 @@ def run_ours(args):
     ctx.synchronize()
     nrec = 20
     ctx.record(4)
+    grp0 = ctx.group_launches
     for _ in range(nrec):
         cf.recurrence_step(A, U, W, p.alpha, p.beta)
         U, W = W, U
     ctx.record(5)
+    grouped = ctx.group_launches - grp0 >= nrec  # which step kernel the library chose
     rec_ms = ctx.elapsed_ms(4, 5) / nrec
     del W
     rec_bytes = recur_step_bytes(Dl, nnz_l, nb)
@@ -317,8 +319,9 @@ def run_ours(args):
             "roofline": {
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "step_tma_kernel<complex, kStepRecur> (V_n-only step: 2 of every 3 "
-                          "filter steps)",
+                "kernel": ("step_group_kernel<complex, kStepRecur> (row-group kernel, band order)"
+                           if grouped else "step_tma_kernel<complex, kStepRecur> (SELL kernel)")
+                          + ": the V_n-only step, 2 of every 3 filter steps",
                 "algorithmic_bytes": rec_bytes,
                 "launch_ms": round(rec_ms, 4),
                 "note": "algorithmic bytes nnz*(16+4) + 3*D*n_b*16 (matrix, U gathered, W read "

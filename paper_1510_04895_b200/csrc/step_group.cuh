@@ -382,6 +382,16 @@ inline Geometry group_geometry(int us) {
     return g;
 }
 
+// band tile order of a row-group launch (set_band_order): slices must be whole tiles
+inline bool group_band_order(const Context& ctx, const Matrix& a, StepParams& p, size_t row_bytes,
+                             int64_t tile_span) {
+    set_band_order(ctx, a, p, kTileRows, row_bytes);
+    if (p.band_tps != 0 && (p.band_plane_chunks % 2 != 0 || p.band_slice_chunks % 2 != 0 ||
+                            (p.band_slice_chunks * 32) % tile_span != 0))
+        p.band_tps = 0;
+    return p.band_tps != 0;
+}
+
 inline const void* find_scaled_grouped(const Matrix& a, double s) {
     for (const auto& e : a.grp.scaled)
         if (e.first == s) return e.second->p;
@@ -415,9 +425,9 @@ bool run_group(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int 
         StepParams probe{};
         probe.row0 = s.row0;
         probe.row1 = s.row1;
-        set_band_order(ctx, a, probe, kTileRows,
-                       static_cast<size_t>(std::min(slab, units)) * sizeof(T));
-        if (probe.band_tps == 0) return false;
+        if (!group_band_order(ctx, a, probe, static_cast<size_t>(std::min(slab, units)) * sizeof(T),
+                              tile_span))
+            return false;
     }
     int used_total = 0;
     for (int u0 = 0; u0 < units; u0 += slab) {
@@ -464,14 +474,8 @@ bool run_group(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int 
         const int64_t need = (((s.row1 + 31) >> 5) - (s.row0 >> 5) + 1) / 2;
         bool band = false;
         if constexpr (DMODE == 0) {
-            if (ctx.tiles_per_cta > 0) {
-                set_band_order(ctx, a, p, kTileRows, static_cast<size_t>(us) * sizeof(T));
-                // band slices must be whole tiles (line groups)
-                if (p.band_tps != 0 && (p.band_plane_chunks % 2 != 0 || p.band_slice_chunks % 2 != 0 ||
-                                        (p.band_slice_chunks * 32) % tile_span != 0))
-                    p.band_tps = 0;
-                band = p.band_tps != 0;
-            }
+            if (ctx.tiles_per_cta > 0)
+                band = group_band_order(ctx, a, p, static_cast<size_t>(us) * sizeof(T), tile_span);
         }
         if (band) kernel = step_group_kernel<CPLX, T, KIND, DMODE, DMODE == 0 ? 1 : 0>;
         static thread_local std::map<std::pair<const void*, int>, size_t> attr_set;

@@ -232,7 +232,8 @@ def test_group_default_takes_the_band_launches(orc, lines):
     try:
         ctx1 = g.ranks[0]
         ctx1.set_option("group_lines", lines)
-        ctx1.set_option("band_bytes", 64 * nb * 16)  # 64-row slices = 2 lattice lines
+        # slices of 2 lattice lines (64 rows), 4 for 4-line tiles
+        ctx1.set_option("band_bytes", 32 * max(lines, 2) * nb * 16)
         spec = cf.LatticeSpec(*l, disorder=0.5, seed=2)
         csr = orc.topological_insulator(*l, disorder=0.5, seed=2)
         A = g.topological_insulator(spec)[0]
