@@ -25,7 +25,9 @@
 #endif
 #ifndef CFD_GRP_MINB
 #define CFD_GRP_MINB 2  // 255 registers per thread (8 warps/SM): a site's 24 gathers, W and
-                        // the hoisted matrix values in flight; 168 / 128 registers spill
+                        // the hoisted matrix values in flight.  168 registers (12 warps/SM,
+                        // ~50 bytes spilled) measured slower in an alternating A/B on one box:
+                        // C4 filter 7.94 vs 7.78 ms per step, X-update steps 10.9 vs 9.5 ms
 #endif
 
 namespace cfd {
