@@ -23,6 +23,10 @@
 #ifndef CFD_GRP_THREADS
 #define CFD_GRP_THREADS 128
 #endif
+#ifndef CFD_GRP_X_EARLY
+#define CFD_GRP_X_EARLY 1  // X rows loaded with W (16 registers) instead of after the products:
+                           // C4 X-update step 9.50 -> 8.87 ms (alternating A/B)
+#endif
 #ifndef CFD_GRP_MINB
 #define CFD_GRP_MINB 2  // 255 registers per thread (8 warps/SM): a site's 24 gathers, W and
                         // the hoisted matrix values in flight.  168 registers (12 warps/SM,
@@ -153,14 +157,18 @@ __global__ void __launch_bounds__(CFD_GRP_THREADS, CFD_GRP_MINB)
         }
         return q;
     };
-    // W now; X / x0 are read after the products (their registers are the gathers' while
-    // those fly) and only start towards the L2 here
-    auto load_w = [&](const Rows& q, T (&wi)[G]) {
+    // W and X now; x0 is read after the products and only starts towards the L2 here
+    auto load_w = [&](const Rows& q, T (&wi)[G], T (&xi)[G]) {
 #pragma unroll
         for (int r = 0; r < G; ++r) {
-            wi[r] = T{};
+            wi[r] = xi[r] = T{};
             if constexpr (kind_reads_w(KIND)) wi[r] = ldst(&W[q.own[r]]);
-            if constexpr (kind_reads_x(KIND)) prefetch_l2(&X[q.own[r]]);
+            if constexpr (kind_reads_x(KIND)) {
+                if constexpr (CFD_GRP_X_EARLY)
+                    xi[r] = ldst(&X[q.own[r]]);
+                else
+                    prefetch_l2(&X[q.own[r]]);
+            }
             if constexpr (DMODE == 2 && KIND != kStepStart2) prefetch_l2(&X0[q.own[r]]);
         }
     };
@@ -267,12 +275,13 @@ __global__ void __launch_bounds__(CFD_GRP_THREADS, CFD_GRP_MINB)
 #pragma unroll
         for (int r = 0; r < G; ++r) ui[r] = ldgk(&inu[q.own[r] + halo * pitch]);
     };
-    auto finish = [&](const Rows& q, const T (&acc)[G], const T (&ui)[G], const T (&wi)[G]) {
-        T xi[G], x0v[G];
+    auto finish = [&](const Rows& q, const T (&acc)[G], const T (&ui)[G], const T (&wi)[G],
+                      T (&xi)[G]) {
+        T x0v[G];
 #pragma unroll
         for (int r = 0; r < G; ++r) {
-            xi[r] = x0v[r] = T{};
-            if constexpr (kind_reads_x(KIND)) xi[r] = ldst(&X[q.own[r]]);
+            x0v[r] = T{};
+            if constexpr (kind_reads_x(KIND) && !CFD_GRP_X_EARLY) xi[r] = ldst(&X[q.own[r]]);
             if constexpr (DMODE == 2 && KIND != kStepStart2) x0v[r] = ldst(&X0[q.own[r]]);
         }
         if constexpr (SACC) {
@@ -328,13 +337,13 @@ __global__ void __launch_bounds__(CFD_GRP_THREADS, CFD_GRP_MINB)
             if (rg >= row1) continue;
             const int4 h = reinterpret_cast<const int4*>(seg)[gi];
             const Rows q = rows_of(rg);
-            T acc[G], ui[G], wi[G];
+            T acc[G], ui[G], wi[G], xi[G];
 #pragma unroll
             for (int r = 0; r < G; ++r) {
                 acc[r] = O::zero();
                 ui[r] = T{};
             }
-            load_w(q, wi);
+            load_w(q, wi, xi);
             if (h.w == 0) {
                 mac_generic(h, seg, vseg, q, acc, ui);
             } else {
@@ -346,7 +355,7 @@ __global__ void __launch_bounds__(CFD_GRP_THREADS, CFD_GRP_MINB)
                 mac_pat(h.w, std::integral_constant<int, 0>{}, gx, vs, acc, ui);
                 mac_pat(h.w, std::integral_constant<int, 1>{}, gy, vs, acc, ui);
             }
-            finish(q, acc, ui, wi);
+            finish(q, acc, ui, wi, xi);
         }
         __syncthreads();  // buffer `buf` is refilled two tiles later
     }
