@@ -247,3 +247,23 @@ def test_group_default_takes_the_band_launches(orc, lines):
         assert bits_equal(X.to_numpy(), xr)
     finally:
         g.close()
+
+
+def test_group_sparse_block_with_exact_zeros(gctx, orc):
+    """Unit-vector columns: most products are exact zeros.  The two-multiply products of the
+    static TI patterns drop the 0 * u terms of purely real / imaginary entries, which only
+    matters for the sign of an exact zero when a whole product is zero; sums start from +0 and
+    round to nearest, so the filtered block still equals the oracle's bits here."""
+    l = (6, 6, 5)
+    A, c = ti(gctx, orc, l)
+    nb = 8
+    x0 = np.zeros((c.dim, nb), dtype=np.complex128)
+    for k in range(nb):
+        x0[(37 * k + 5) % c.dim, k] = 1.0 if k % 2 == 0 else -1.0j
+    p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 9, "lanczos2")
+    X = block(A, x0)
+    before = gctx.group_launches
+    cf.apply_filter(A, X, p)
+    assert gctx.group_launches > before
+    xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
+    assert bits_equal(X.to_numpy(), xr)
