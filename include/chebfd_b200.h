@@ -107,7 +107,17 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_PAIR_SLAB = 11, CHEBFD_OPT_MOMENTS = 12, CHEBFD_OPT_PDL = 14,
        CHEBFD_OPT_DELAYED_X = 15, CHEBFD_OPT_BAND_BYTES = 16, CHEBFD_OPT_ASYNC_START = 17,
        CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19, CHEBFD_OPT_GRAM = 20,
-       CHEBFD_OPT_GROUPED = 21, CHEBFD_OPT_GROUP_LINES = 22 };
+       CHEBFD_OPT_GROUPED = 21, CHEBFD_OPT_GROUP_LINES = 22, CHEBFD_OPT_RING = 23,
+       CHEBFD_OPT_RING_SEGX = 24, CHEBFD_OPT_RING_NO = 25, CHEBFD_OPT_RING_NZ = 26 };
+/* CHEBFD_OPT_RING: the site-ring step kernel (csrc/step_ring.cuh) on complex TI lattice
+ * operators with blocks of a multiple of 32 columns: a producer warp stages each x-column of
+ * a strip of four lattice lines (site blocks, z -+ 1 rows, matrix values) in shared-memory
+ * rings by TMA bulk copies, consumer warps multiply straight from shared memory, so a site
+ * block crosses L2 -> SM about once instead of once per referencing site.  Dot-free fused /
+ * V_n-only steps; W and X bit-identical to the other step kernels.  1: the launches the
+ * row-group kernel would take (band order); 2: every applicable launch; 0: off.
+ * CHEBFD_OPT_RING_SEGX (x-columns per CTA, default 64), _NO / _NZ (ring depths, default
+ * 5 / 3). */
 /* CHEBFD_OPT_GROUPED (default 1): dot-free steps that run in the band tile order (lattice
  * operators whose z-planes exceed the L2 budget, CHEBFD_OPT_BAND_BYTES) use the row-group
  * kernel: four consecutive rows -- a lattice site's orbitals -- share one merged list of
@@ -160,6 +170,8 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
 int chebfd_ctx_band_launches(chebfd_ctx* ctx, int64_t* count);
 /* step launches that ran the row-group kernel (CHEBFD_OPT_GROUPED) so far */
 int chebfd_ctx_group_launches(chebfd_ctx* ctx, int64_t* count);
+/* step launches that ran the site-ring kernel (CHEBFD_OPT_RING) so far */
+int chebfd_ctx_ring_launches(chebfd_ctx* ctx, int64_t* count);
 int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value);
 
 /* CUDA-event timing on the context stream: 16 event slots per context. */

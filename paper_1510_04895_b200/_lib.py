@@ -92,6 +92,7 @@ _SIGS = {
     "chebfd_ctx_set_option": (_int, [_vp, _int, _i64]),
     "chebfd_ctx_band_launches": (_int, [_vp, _vp]),
     "chebfd_ctx_group_launches": (_int, [_vp, _vp]),
+    "chebfd_ctx_ring_launches": (_int, [_vp, _vp]),
     "chebfd_ctx_event_record": (_int, [_vp, _int]),
     "chebfd_ctx_event_elapsed": (_int, [_vp, _int, _int, _vp]),
     "chebfd_host_alloc": (_int, [C.c_size_t, _pp]),

@@ -160,6 +160,13 @@ class Context:
         return v.value
 
     @property
+    def ring_launches(self) -> int:
+        """Step launches that ran the site-ring kernel (option "ring")."""
+        v = C.c_int64()
+        _check(_lib().chebfd_ctx_ring_launches(self._h, C.byref(v)))
+        return v.value
+
+    @property
     def band_launches(self) -> int:
         """Step launches that ran in the band (2.5D) tile order."""
         v = C.c_int64()
@@ -185,7 +192,8 @@ class Context:
                 "pair_tile_rows": 7, "pair_threads": 8, "pair_extra": 9, "pair_hints": 10,
                 "pair_slab": 11, "moments": 12, "pdl": 14, "delayed_x": 15,
                 "band_bytes": 16, "async_start": 17, "tiles_per_cta": 18,
-                "compact_halo": 19, "gram": 20, "grouped": 21, "group_lines": 22}[name]
+                "compact_halo": 19, "gram": 20, "grouped": 21, "group_lines": 22,
+                "ring": 23, "ring_segx": 24, "ring_no": 25, "ring_nz": 26}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):

@@ -910,6 +910,7 @@ static void ctx_init(Context& c, int device) {
     // test hook: CHEBFD_GROUPED=2 runs the whole suite on the row-group kernel
     if (const char* e = std::getenv("CHEBFD_GROUPED")) c.grouped = std::atoi(e);
     if (const char* e = std::getenv("CHEBFD_GROUP_LINES")) c.group_lines = std::atoi(e);
+    if (const char* e = std::getenv("CHEBFD_RING")) c.ring = std::atoi(e);
     ctx_sync(c);
 }
 
@@ -1015,6 +1016,10 @@ int chebfd_ctx_group_launches(chebfd_ctx* ctx, int64_t* count) {
     return guard([&] { *count = reinterpret_cast<Context*>(ctx)->group_launches; });
 }
 
+int chebfd_ctx_ring_launches(chebfd_ctx* ctx, int64_t* count) {
+    return guard([&] { *count = reinterpret_cast<Context*>(ctx)->ring_launches; });
+}
+
 int chebfd_ctx_band_launches(chebfd_ctx* ctx, int64_t* count) {
     return guard([&] { *count = reinterpret_cast<Context*>(ctx)->band_launches; });
 }
@@ -1060,6 +1065,14 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->grouped = static_cast<int>(value);
         else if (option == CHEBFD_OPT_GROUP_LINES)
             c->group_lines = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING)
+            c->ring = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_SEGX)
+            c->ring_segx = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_NO)
+            c->ring_no = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_NZ)
+            c->ring_nz = static_cast<int>(value);
         else if (option == CHEBFD_OPT_TILES_PER_CTA)
             c->tiles_per_cta = static_cast<int>(std::max<int64_t>(value, 0));
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)

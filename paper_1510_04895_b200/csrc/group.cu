@@ -244,7 +244,81 @@ __global__ void scale_kernel(double* __restrict__ out, const double* __restrict_
         out[i] = __dmul_rn(in[i], s);
 }
 
+
+// ---- site-ring plan (step_ring.cuh) ---------------------------------------------------
+// static site of pattern P: its x -+ 1 / y -+ 1 column blocks are the lattice neighbours' rows
+template <class P>
+__device__ bool ring_neighbours_ok(const int* c, int64_t own0, int64_t line_rows) {
+    for (int r = 0; r < kGroupRows; ++r) {
+        if (static_cast<int64_t>(c[P::OWN - 8 + r] & kColMask) != own0 - line_rows + r) return false;
+        if (static_cast<int64_t>(c[P::OWN - 4 + r] & kColMask) != own0 - kGroupRows + r) return false;
+        if (static_cast<int64_t>(c[P::OWN + 4 + r] & kColMask) != own0 + kGroupRows + r) return false;
+        if (static_cast<int64_t>(c[P::OWN + 8 + r] & kColMask) != own0 + line_rows + r) return false;
+    }
+    return true;
+}
+
+__global__ void ring_plan_kernel(const int64_t* __restrict__ tile_cptr,
+                                 const int64_t* __restrict__ tile_vptr, const int* __restrict__ cols,
+                                 int64_t ngroups, int64_t halo_lo, int64_t line_rows,
+                                 int4* __restrict__ plan, int* __restrict__ bad) {
+    const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (g >= ngroups) return;
+    const int64_t t = g / kTileGroups;
+    const int gi = static_cast<int>(g % kTileGroups);
+    const int* seg = cols + tile_cptr[t];
+    const int4 h = reinterpret_cast<const int4*>(seg)[gi];
+    const int* c = seg + h.x;
+    int nv = 0;
+    for (int k = 0; k < h.z; ++k) nv += __popc(static_cast<unsigned>(c[k]) >> kColBits);
+    if (nv > kRingMaxVals) atomicExch(bad, 1);
+    const int64_t voff = tile_vptr[t] + h.y;
+    const int64_t own0 = g * kGroupRows + halo_lo;
+    int4 a;
+    bool ok = true;
+    if (h.w == 1) {
+        a = make_int4(c[0] & kColMask, c[1] & kColMask, c[22] & kColMask, c[23] & kColMask);
+        ok = ring_neighbours_ok<PatTiMid>(c, own0, line_rows);
+    } else if (h.w == 2) {
+        a = make_int4(-1, -1, c[20] & kColMask, c[21] & kColMask);
+        ok = ring_neighbours_ok<PatTiLo>(c, own0, line_rows);
+    } else if (h.w == 3) {
+        a = make_int4(c[0] & kColMask, c[1] & kColMask, -1, -1);
+        ok = ring_neighbours_ok<PatTiHi>(c, own0, line_rows);
+    } else {
+        const int64_t coff = tile_cptr[t] + h.x;
+        a = make_int4(static_cast<int>(coff & 0xFFFFFFFFll), static_cast<int>(coff >> 32), h.z, 0);
+    }
+    if (!ok) atomicExch(bad, 1);
+    plan[2 * g] = a;
+    plan[2 * g + 1] =
+        make_int4(static_cast<int>(voff & 0xFFFFFFFFll), static_cast<int>(voff >> 32), h.w, nv);
+}
+
 }  // namespace
+
+// plan of the site-ring step kernel: complex lattice operators whose rows are whole sites in
+// linear tiles; leaves gm.ring_ok = false where it does not apply
+static void build_ring_plan(Matrix& m, cudaStream_t st) {
+    GroupedMatrix& gm = m.grp;
+    gm.ring_ok = false;
+    const int64_t rows = m.part.local;
+    if (!gm.ok || !m.kind || m.line_rows <= 0 || m.plane_rows <= 0 || gm.il_line_rows != 0 ||
+        m.line_rows % kGroupRows != 0 || m.plane_rows % m.line_rows != 0 || rows % m.plane_rows != 0)
+        return;
+    const int64_t ngroups = rows / kGroupRows;
+    gm.ring_plan.ensure(sizeof(int4) * 2 * ngroups);
+    DeviceBuffer bad(sizeof(int));
+    CFD_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    ring_plan_kernel<<<static_cast<unsigned>((ngroups + 127) / 128), 128, 0, st>>>(
+        gm.tile_cptr.as<int64_t>(), gm.tile_vptr.as<int64_t>(), gm.cols.as<int>(), ngroups,
+        m.part.halo_lo, m.line_rows, gm.ring_plan.as<int4>(), bad.as<int>());
+    CFD_CUDA(cudaGetLastError());
+    int h = 0;
+    CFD_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CFD_CUDA(cudaStreamSynchronize(st));
+    gm.ring_ok = h == 0;
+}
 
 void build_grouped(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d_cols,
                    const void* d_vals, cudaStream_t st) {
@@ -322,6 +396,7 @@ void build_grouped(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t
     CFD_CUDA(cudaGetLastError());
     CFD_CUDA(cudaStreamSynchronize(st));
     gm.ok = true;
+    build_ring_plan(m, st);
 }
 
 // values of the grouped form pre-multiplied by s (kept beside Matrix::scaled, same keys)

@@ -138,7 +138,16 @@ struct GroupedMatrix {
     int64_t il_line_rows = 0;
     int il_lines = 1;
     std::vector<std::pair<double, std::unique_ptr<DeviceBuffer>>> scaled;
+    // Site-ring plan (step_ring.cuh; complex lattice operators with linear tiles): two int4
+    // per group -- static-pattern sites: (z-1 row a, z-1 row b, z+1 row a, z+1 row b)
+    // extended-row indices or -1; generic sites: (column-list offset lo, hi, padded column
+    // count, 0) -- then (value offset lo, hi, pattern id, value count).  ring_ok: every
+    // static site's x / y neighbour columns are its lattice neighbours' rows and no site
+    // holds more than kRingMaxVals values.
+    bool ring_ok = false;
+    DeviceBuffer ring_plan;
 };
+constexpr int kRingMaxVals = 44;  // values per site staged by the site-ring kernel
 
 struct Matrix {
     Context* ctx = nullptr;
@@ -275,6 +284,11 @@ struct Context {
     int group_lines = 1;  // lattice lines per tile of the grouped form (1: linear); set before
                           // building matrices (CHEBFD_OPT_GROUP_LINES)
     int64_t group_launches = 0;  // step launches that ran the row-group kernel
+    // site-ring step kernel (step_ring.cuh): 0 off, 1 where the row-group kernel would run
+    // (band-ordered launches), 2 wherever it applies; CHEBFD_OPT_RING.  ring_segx / ring_no /
+    // ring_nz: x-columns per CTA and ring depths (0: defaults); CHEBFD_OPT_RING_SEGX / _NO / _NZ
+    int ring = 0, ring_segx = 0, ring_no = 0, ring_nz = 0;
+    int64_t ring_launches = 0;   // step launches that ran the site-ring kernel
     // exchange only the referenced halo rows of structurally symmetric operators (lattice
     // models, bitwise-Hermitian from_csr input); CHEBFD_OPT_COMPACT_HALO
     bool compact_halo = true;
@@ -349,6 +363,8 @@ void launch_step_r1(Context& ctx, const StepArgs& s, cudaStream_t st, int units,
 bool launch_group_c(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
 bool launch_group_r2(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
 bool launch_group_r1(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
+// site-ring step kernel (step_ringc.cu): false = does not apply to this launch
+bool launch_ring_c(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch);
 // group gi of tile t of a grouped matrix -> its first row (linear or line-interleaved tiles)
 struct TileMap {
     int64_t line_rows;  // 0: linear

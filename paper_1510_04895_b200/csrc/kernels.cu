@@ -341,6 +341,7 @@ void launch_step(Context& ctx, const StepArgs& s, cudaStream_t st) {
     const int64_t width = s.width_cols;
     // the row-group kernel where the grouped form applies, else the SELL kernels
     if (kind == CHEBFD_COMPLEX128) {
+        if (launch_ring_c(ctx, s, st, static_cast<int>(width), static_cast<int>(width))) return;
         if (!launch_group_c(ctx, s, st, static_cast<int>(width), static_cast<int>(width)))
             launch_step_c(ctx, s, st, static_cast<int>(width), static_cast<int>(width));
     } else if (width % 2 == 0) {

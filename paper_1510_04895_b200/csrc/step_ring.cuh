@@ -1,0 +1,491 @@
+// Site-ring step kernel (sm_100a): a warp-specialised Chebyshev step for topological-insulator
+// lattice operators (complex blocks of 32 or 64 units per row / column slab).
+//
+// Why: the row-group kernel (step_group.cuh) gathers a site's 24 neighbour rows through the
+// L1 with 255 registers per thread -- 8 warps per SM, whose loads and FP64 work do not
+// overlap, and ~22 KB per site crossing the L2 -> SM path (L1 hit rate 21 %).  Here the
+// gathered operand never touches a register before it is multiplied:
+//
+//   * a CTA owns a strip of SY = 4 adjacent lattice lines of one z-plane and marches along x;
+//   * one PRODUCER warp copies, per x-column, the strip's site blocks (SY + 2 sites of the
+//     own plane: the strip and its y -+ 1 halo sites) and the z -+ 1 rows + matrix values of
+//     the column's sites into shared-memory rings with TMA bulk copies
+//     (cp.async.bulk ... mbarrier::complete_tx), several columns ahead;
+//   * CONSUMER warps (one 16-byte unit of a site's four rows per thread, as the row-group
+//     kernel) read every operand from shared memory: x -+ 1 neighbours are the neighbouring
+//     ring slots, y -+ 1 neighbours the neighbouring lines' slots, so a site block crosses
+//     L2 -> SM once per strip (+ halo) instead of once per referencing site:
+//     ~10.7 KB per site instead of ~22 KB;
+//   * full / empty mbarriers per ring slot; no __syncthreads after the roles split.
+//
+// Each row still meets its entries in CSR order with the reference's roundings (the static
+// site patterns of group_patterns.hpp; x / y wrap sites take a generic path that gathers
+// from global memory), so W and X are bit-identical to the other step kernels.
+//
+// The producer's addresses come from a per-site plan built with the grouped form
+// (group.cu build_ring_plan): the z -+ 1 row indices (extended rows, so compact halos and
+// rank boundaries need nothing special), the site's value offset and pattern id.  x / y
+// neighbours of static sites are checked there to be the lattice neighbours.
+#pragma once
+#include <utility>
+
+#include "group_patterns.hpp"
+#include "step_kernels.cuh"
+
+namespace cfd {
+namespace {
+
+constexpr int kRingSY = 4;         // lattice lines per strip
+constexpr int kRingMaxDepth = 8;   // ring slots (each ring)
+
+struct RingParams {
+    const int4* plan;   // two int4 per site (group.cu)
+    const int* cols;    // grouped columns (generic sites)
+    const void* vals;   // grouped values pre-multiplied by alpha
+    int lx, ly;         // sites per line, lines per plane
+    int planes;         // planes of this launch
+    int segx, nseg;     // x-columns per CTA, segments per line
+    int spb;            // strips per band (band order of the grid)
+    int no, nz;         // ring depths: own-plane columns, z / value stages
+    int full;           // 1: the slab is the whole row (a site's four rows are one copy)
+};
+
+template <class F, int... I>
+__device__ __forceinline__ void ring_for_impl(F&& f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void ring_for(F&& f) {
+    ring_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, unsigned bytes,
+                                                 uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+        "[%3], %4;\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// shared-memory bases of a site's operand classes (unit offset included)
+struct RingBases {
+    const unsigned char *zlo, *ym, *xm, *own, *xp, *yp, *zhi;
+};
+
+// operand k of pattern P: columns run z-1 | y-1 | x-1 | site | x+1 | y+1 | z+1
+template <class P, int K, int RB>
+__device__ __forceinline__ double2 ring_operand(const RingBases& b) {
+    constexpr int ZLO = P::OWN - 8;  // z-1 columns in front (2 or 0)
+    constexpr int q = K - ZLO;
+    const unsigned char* a;
+    if constexpr (K < ZLO)
+        a = b.zlo + K * RB;
+    else if constexpr (q < 4)
+        a = b.ym + q * RB;
+    else if constexpr (q < 8)
+        a = b.xm + (q - 4) * RB;
+    else if constexpr (q < 12)
+        a = b.own + (q - 8) * RB;
+    else if constexpr (q < 16)
+        a = b.xp + (q - 12) * RB;
+    else if constexpr (q < 20)
+        a = b.yp + (q - 16) * RB;
+    else
+        a = b.zhi + (q - 20) * RB;
+    return *reinterpret_cast<const double2*>(a);
+}
+
+template <class P, int RB>
+__device__ __forceinline__ void ring_mac(const RingBases& b, const double2* vs, double2 (&acc)[4],
+                                         double2 (&ui)[4]) {
+    using O = Ops<true, double2>;
+    ring_for<P::NC>([&](auto kt) {
+        constexpr int k = decltype(kt)::value;
+        const double2 gk = ring_operand<P, k, RB>(b);
+        ring_for<kGroupRows>([&](auto rt) {
+            constexpr int r = decltype(rt)::value;
+            if constexpr ((P::m(k) >> r) & 1u) {
+                if constexpr ((P::re(k) >> r) & 1u) {
+                    const double v = vs[P::voff(k, r)].x;
+                    acc[r].x = add(acc[r].x, mul(v, gk.x));
+                    acc[r].y = add(acc[r].y, mul(v, gk.y));
+                } else if constexpr ((P::im(k) >> r) & 1u) {
+                    const double v = vs[P::voff(k, r)].y;
+                    acc[r].x = sub(acc[r].x, mul(v, gk.y));
+                    acc[r].y = add(acc[r].y, mul(v, gk.x));
+                } else {
+                    acc[r] = O::vadd(acc[r], O::prod(vs[P::voff(k, r)], gk));
+                }
+            }
+        });
+        if constexpr (k >= P::OWN && k < P::OWN + kGroupRows) ui[k - P::OWN] = gk;
+    });
+}
+
+template <int KIND, int US>
+__global__ void __launch_bounds__(kRingSY* US + 32, 1)
+    step_ring_kernel(const StepParams p, const RingParams rp) {
+    using T = double2;
+    using O = Ops<true, double2>;
+    using M = double2;
+    constexpr int SY = kRingSY;
+    constexpr int G = kGroupRows;
+    constexpr int RB = US * 16;                     // bytes of a row (slab)
+    constexpr int OS = (SY + 2) * G * RB;           // own-plane column slot
+    constexpr int VB = kRingMaxVals * 16;           // value bytes per site
+    constexpr int ZS = SY * G * RB + SY * VB;       // z-row + value stage
+    constexpr int NCT = SY * US;                    // consumer threads
+    constexpr int NCW = NCT / 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[4 * kRingMaxDepth];
+    uint64_t* full_o = bars;
+    uint64_t* empty_o = bars + kRingMaxDepth;
+    uint64_t* full_z = bars + 2 * kRingMaxDepth;
+    uint64_t* empty_z = bars + 3 * kRingMaxDepth;
+    const int t = threadIdx.x;
+    const int no = rp.no, nz = rp.nz;
+    unsigned char* oring = smem_raw;
+    unsigned char* zring = oring + static_cast<size_t>(no) * OS;
+    int4* plan_s = reinterpret_cast<int4*>(zring + static_cast<size_t>(nz) * ZS);
+
+    // CTA -> (band of strips, plane, strip in the band, x segment): planes innermost over a
+    // band, so the z -+ 1 rows a strip reads were own rows of a CTA a band slice earlier
+    unsigned idx = blockIdx.x;
+    const int q = static_cast<int>(idx % static_cast<unsigned>(rp.nseg));
+    idx /= static_cast<unsigned>(rp.nseg);
+    const int sb = static_cast<int>(idx % static_cast<unsigned>(rp.spb));
+    idx /= static_cast<unsigned>(rp.spb);
+    const int z = static_cast<int>(idx % static_cast<unsigned>(rp.planes));
+    const int band = static_cast<int>(idx / static_cast<unsigned>(rp.planes));
+    const int lx = rp.lx, ly = rp.ly, segx = rp.segx;
+    const int y0 = (band * rp.spb + sb) * SY;
+    const int xa = q * segx;
+    const int xb = min(lx, xa + segx);
+    const int jlo = xa > 0 ? xa - 1 : xa;  // own-plane columns [jlo, jhi): the segment + aprons
+    const int jhi = xb < lx ? xb + 1 : xb;
+    // owned site index of (x = 0, line y0) of this plane
+    const int64_t site0 = (p.row0 >> 2) + (static_cast<int64_t>(z) * ly + y0) * lx;
+
+    // the segment's plan -> shared memory (matrix data: may precede the previous kernel's end)
+    {
+        const int n2 = 2 * (xb - xa);
+        for (int i = t; i < SY * 2 * segx; i += blockDim.x) {
+            const int l = i / (2 * segx), r = i - l * 2 * segx;
+            if (r < n2) plan_s[i] = __ldg(&rp.plan[2 * (site0 + static_cast<int64_t>(l) * lx + xa) + r]);
+        }
+    }
+    if (t == 0) {
+        for (int i = 0; i < no; ++i) {
+            mbar_init(&full_o[i], 1);
+            mbar_init(&empty_o[i], NCW);
+        }
+        for (int i = 0; i < nz; ++i) {
+            mbar_init(&full_z[i], 1);
+            mbar_init(&empty_z[i], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int pitch = p.pitch;
+
+    if (t >= NCT) {
+        // ================================ producer warp ================================
+        const int lane = t - NCT;
+        const T* inb = static_cast<const T*>(p.in) + p.u_off;
+        const M* gvals = static_cast<const M*>(rp.vals);
+        const uint64_t pol_keep = l2_make_policy(1);
+        const uint64_t pol_stream = l2_make_policy(2);
+        const int K = jhi - jlo;
+        for (int k = 0; k <= K; ++k) {
+            if (k < K) {
+                const int j = jlo + k, slot = k % no;
+                if (k >= no) mbar_wait(&empty_o[slot], ((k / no) - 1) & 1);
+                const bool apron = j < xa || j >= xb;
+                int ss, rr;
+                unsigned bytes;
+                bool active;
+                if (rp.full) {
+                    ss = lane;
+                    rr = 0;
+                    bytes = G * RB;
+                    active = lane < SY + 2;
+                } else {
+                    ss = lane >> 2;
+                    rr = lane & 3;
+                    bytes = RB;
+                    active = lane < G * (SY + 2);
+                }
+                const int y = y0 + ss - 1;
+                active = active && y >= 0 && y < ly && (!apron || (ss >= 1 && ss <= SY));
+                const unsigned total = __reduce_add_sync(0xffffffffu, active ? bytes : 0u);
+                if (lane == 0) mbar_arrive_expect_tx(&full_o[slot], total);
+                __syncwarp();
+                if (active) {
+                    const int64_t erow =
+                        p.halo_lo + G * (site0 + static_cast<int64_t>(ss - 1) * lx + j) + rr;
+                    tma_load_1d_hint(oring + static_cast<size_t>(slot) * OS + (ss * G + rr) * RB,
+                                     inb + erow * pitch, bytes, &full_o[slot], pol_keep);
+                }
+            }
+            const int c = jlo + k - 1;
+            if (c >= xa && c < xb) {
+                const int kz = c - xa, slot = kz % nz;
+                if (kz >= nz) mbar_wait(&empty_z[slot], ((kz / nz) - 1) & 1);
+                unsigned bytes = 0;
+                const void* src = nullptr;
+                unsigned char* dst = zring + static_cast<size_t>(slot) * ZS;
+                bool keep = true;
+                if (lane < G * SY) {
+                    const int l = lane >> 2, w = lane & 3;
+                    const int4 a = plan_s[(l * segx + kz) * 2];
+                    const int4 b = plan_s[(l * segx + kz) * 2 + 1];
+                    const int row = w == 0 ? a.x : (w == 1 ? a.y : (w == 2 ? a.z : a.w));
+                    if (b.z != 0 && row >= 0) {
+                        bytes = RB;
+                        src = inb + static_cast<int64_t>(row) * pitch;
+                        dst += (l * G + w) * RB;
+                    }
+                } else if (lane < (G + 1) * SY) {
+                    const int l = lane - G * SY;
+                    const int4 b = plan_s[(l * segx + kz) * 2 + 1];
+                    const int64_t voff = static_cast<int64_t>(static_cast<unsigned>(b.x)) |
+                                         (static_cast<int64_t>(b.y) << 32);
+                    bytes = static_cast<unsigned>(b.w) * 16u;
+                    src = gvals + voff;
+                    dst += SY * G * RB + l * VB;
+                    keep = false;
+                }
+                const unsigned total = __reduce_add_sync(0xffffffffu, bytes);
+                if (lane == 0) mbar_arrive_expect_tx(&full_z[slot], total);
+                __syncwarp();
+                if (bytes) tma_load_1d_hint(dst, src, bytes, &full_z[slot], keep ? pol_keep : pol_stream);
+            }
+        }
+    } else {
+        // ================================ consumer warps ================================
+        const int l = t / US, u = t - l * US;
+        const int cu = p.u_off + u;
+        const bool lane0 = (t & 31) == 0;
+        const T* __restrict__ inu = static_cast<const T*>(p.in) + cu;
+        T* __restrict__ W = static_cast<T*>(p.w) + cu;
+        T* __restrict__ X = static_cast<T*>(p.x) + cu;
+        double coeff = p.c0, c1 = p.c1, c2 = p.c2;
+        if (kind_fused(KIND) && p.coeff_dev) coeff = p.coeff_dev[p.coeff_index];
+        if ((KIND == kStepFusedX2 || KIND == kStepFusedX3) && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
+        if (KIND == kStepFusedX3 && p.coeff_dev) c2 = p.coeff_dev[p.coeff_index - 2];
+        const uint64_t pol_stream = l2_make_policy(2);
+        double dummy_a[1] = {0.0}, dummy_c[1] = {0.0};
+        int kw = 0;  // own-plane columns waited for so far
+        for (int c = xa; c < xb; ++c) {
+            const int kz = c - xa;
+            const int64_t rg = G * (site0 + static_cast<int64_t>(l) * lx + c);
+            // own-row streams first: their latency overlaps the barrier waits
+            T wi[G], xi[G];
+            int64_t own[G];
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                own[r] = (rg + r) * pitch;
+                wi[r] = xi[r] = T{};
+                if constexpr (kind_reads_w(KIND)) wi[r] = lds_pol(&W[own[r]], pol_stream);
+                if constexpr (kind_reads_x(KIND)) xi[r] = lds_pol(&X[own[r]], pol_stream);
+            }
+            const int need = min(c + 1, jhi - 1) - jlo;
+            while (kw <= need) {
+                mbar_wait(&full_o[kw % no], (kw / no) & 1);
+                ++kw;
+            }
+            mbar_wait(&full_z[kz % nz], (kz / nz) & 1);
+            const int4 pb = plan_s[(l * segx + kz) * 2 + 1];
+            const unsigned char* oc = oring + static_cast<size_t>((c - jlo) % no) * OS + u * 16;
+            const unsigned char* om = oring + static_cast<size_t>((c - 1 - jlo + no) % no) * OS + u * 16;
+            const unsigned char* op = oring + static_cast<size_t>((c + 1 - jlo) % no) * OS + u * 16;
+            const unsigned char* zb = zring + static_cast<size_t>(kz % nz) * ZS;
+            const M* vs = reinterpret_cast<const M*>(zb + SY * G * RB + l * VB);
+            RingBases b;
+            b.ym = oc + l * (G * RB);
+            b.own = oc + (l + 1) * (G * RB);
+            b.yp = oc + (l + 2) * (G * RB);
+            b.xm = om + (l + 1) * (G * RB);
+            b.xp = op + (l + 1) * (G * RB);
+            b.zlo = zb + l * (G * RB) + u * 16;
+            b.zhi = b.zlo + 2 * RB;
+            T acc[G], ui[G];
+#pragma unroll
+            for (int r = 0; r < G; ++r) acc[r] = O::zero();
+            const int pat = pb.z;
+            if (pat == 1) {
+                ring_mac<PatTiMid, RB>(b, vs, acc, ui);
+            } else if (pat == 2) {
+                ring_mac<PatTiLo, RB>(b, vs, acc, ui);
+            } else if (pat == 3) {
+                ring_mac<PatTiHi, RB>(b, vs, acc, ui);
+            } else {
+                // generic site (x / y wrap, open edges): merged columns gathered from global
+                const int4 pa = plan_s[(l * segx + kz) * 2];
+                const int64_t coff = static_cast<int64_t>(static_cast<unsigned>(pa.x)) |
+                                     (static_cast<int64_t>(pa.y) << 32);
+                const int* cl = rp.cols + coff;
+                const int n = pa.z;
+                int vi = 0;
+#pragma unroll 4
+                for (int k = 0; k < n; ++k) {
+                    const unsigned cw = static_cast<unsigned>(__ldg(cl + k));
+                    const unsigned m = cw >> 28;
+                    const T g = ldg(&inu[static_cast<int64_t>(cw & 0x0FFFFFFFu) * pitch]);
+#pragma unroll
+                    for (int r = 0; r < G; ++r)
+                        if (m & (1u << r)) {
+                            acc[r] = O::vadd(acc[r], O::prod(vs[vi], g));
+                            ++vi;
+                        }
+                }
+#pragma unroll
+                for (int r = 0; r < G; ++r) ui[r] = *reinterpret_cast<const T*>(b.own + r * RB);
+            }
+#pragma unroll
+            for (int r = 0; r < G; ++r)
+                step_epilogue<O, T, KIND, 0>(acc[r], ui[r], wi[r], xi[r], T{}, own[r], W, X,
+                                             static_cast<T*>(nullptr), p.beta, coeff, c1, c2,
+                                             dummy_a, dummy_c);
+            __syncwarp();
+            if (lane0) {
+                mbar_arrive(&empty_z[kz % nz]);
+                if (c - 1 >= jlo) mbar_arrive(&empty_o[(c - 1 - jlo) % no]);
+            }
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline const void* ring_scaled_values(const Matrix& a, double s) {
+    if (s == 1.0) return a.grp.vals.p;
+    for (const auto& e : a.grp.scaled)
+        if (e.first == s) return e.second->p;
+    return nullptr;
+}
+
+// Launch the site-ring kernel for s if it applies; false = nothing launched.
+template <int KIND>
+bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
+    const Matrix& a = *s.a;
+    const GroupedMatrix& gm = a.grp;
+    constexpr int SY = kRingSY;
+    if (ctx.ring == 0 || ctx.kernel_variant != 1 || !gm.ok || !gm.ring_ok) return false;
+    if (s.dots_mode != 0 || units % 32 != 0) return false;
+    const int64_t P = a.plane_rows, Ln = a.line_rows;
+    const int64_t nrows = s.row1 - s.row0;
+    if (P <= 0 || Ln <= 0 || nrows <= 0 || s.row0 % P != 0 || nrows % P != 0) return false;
+    const int64_t lx = Ln / kGroupRows, ly = P / Ln, planes = nrows / P;
+    if (ly % SY != 0 || lx < 1 || lx > (1 << 24) || ly > (1 << 24)) return false;
+    const void* svals = ring_scaled_values(a, s.alpha);
+    if (!svals) return false;
+    const int us = units % 64 == 0 ? 64 : 32;
+    // default (CHEBFD_OPT_RING = 1): where the row-group kernel would run, i.e. the
+    // band-ordered launches (planes beyond the L2 budget); 2: wherever it applies
+    if (ctx.ring == 1) {
+        if (ctx.grouped == 0 || ctx.tiles_per_cta <= 0) return false;
+        StepParams probe{};
+        probe.row0 = s.row0;
+        probe.row1 = s.row1;
+        set_band_order(ctx, a, probe, kTileRows, static_cast<size_t>(std::min(units, 128)) * 16);
+        if (probe.band_tps == 0) return false;
+    }
+    const size_t rb = static_cast<size_t>(us) * 16;
+    const size_t os = (SY + 2) * kGroupRows * rb, zs = SY * kGroupRows * rb + SY * kRingMaxVals * 16;
+    const int segx = static_cast<int>(std::min<int64_t>(lx, ctx.ring_segx > 0 ? ctx.ring_segx : 64));
+    const size_t plan_b = static_cast<size_t>(SY) * segx * 32;
+    int no = us == 64 ? 5 : 5, nz = 3;
+    if (ctx.ring_no > 0) no = std::min(ctx.ring_no, kRingMaxDepth);
+    if (ctx.ring_nz > 0) nz = std::min(ctx.ring_nz, kRingMaxDepth);
+    if (no < 4 || nz < 2) return false;
+    const size_t smem = no * os + nz * zs + plan_b;
+    if (smem > 220 * 1024) return false;
+    // strips per band: the band's slice of the gathered operand within the band budget
+    const int64_t strips = ly / SY;
+    int64_t spb = 1;
+    for (int64_t d = 1; d <= strips; ++d)
+        if (strips % d == 0 && static_cast<size_t>(d * SY * Ln) * units * 16 <=
+                                   static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 1)))
+            spb = d;
+    const int64_t nseg = (lx + segx - 1) / segx;
+    const int64_t grid = strips * planes * nseg;
+    if (grid >= (int64_t(1) << 31)) return false;
+    auto kernel = us == 64 ? step_ring_kernel<KIND, 64> : step_ring_kernel<KIND, 32>;
+    static thread_local std::map<std::pair<const void*, int>, size_t> attr_set;
+    auto& cur = attr_set[std::make_pair(reinterpret_cast<const void*>(kernel), ctx.device)];
+    if (cur < smem) {
+        CFD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        cur = smem;
+    }
+    for (int u0 = 0; u0 < units; u0 += us) {
+        StepParams p{};
+        p.row0 = s.row0;
+        p.row1 = s.row1;
+        p.halo_lo = a.part.halo_lo;
+        p.pitch = pitch;
+        p.u_off = u0;
+        p.US = us;
+        p.in = s.in;
+        p.w = s.w;
+        p.x = s.x;
+        p.x0 = s.x0;
+        p.alpha = s.alpha;
+        p.beta = s.beta;
+        p.c0 = s.c0;
+        p.c1 = s.c1;
+        p.c2 = s.c2;
+        p.coeff_dev = s.coeff_dev;
+        p.coeff_index = s.coeff_index;
+        RingParams rp{};
+        rp.plan = gm.ring_plan.as<int4>();
+        rp.cols = gm.cols.as<int>();
+        rp.vals = svals;
+        rp.lx = static_cast<int>(lx);
+        rp.ly = static_cast<int>(ly);
+        rp.planes = static_cast<int>(planes);
+        rp.segx = segx;
+        rp.nseg = static_cast<int>(nseg);
+        rp.spb = static_cast<int>(spb);
+        rp.no = no;
+        rp.nz = nz;
+        rp.full = (us == units && pitch == units) ? 1 : 0;
+        const bool pdl = s.pdl_ok && ctx.pdl == 2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(static_cast<unsigned>(SY * us + 32));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CFD_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, rp));
+        CFD_CUDA(cudaGetLastError());
+        ctx.launches++;
+        ctx.ring_launches++;
+        ctx.band_launches++;
+    }
+    if (s.grid_used) *s.grid_used = static_cast<int>(grid);
+    return true;
+}
+
+inline bool dispatch_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
+    if (s.dots_mode != 0) return false;
+    switch (s.kind_step) {
+        case kStepFused: return run_ring<kStepFused>(ctx, s, st, units, pitch);
+        case kStepRecur: return run_ring<kStepRecur>(ctx, s, st, units, pitch);
+        case kStepFusedX2: return run_ring<kStepFusedX2>(ctx, s, st, units, pitch);
+        case kStepFusedX3: return run_ring<kStepFusedX3>(ctx, s, st, units, pitch);
+    }
+    return false;
+}
+
+}  // namespace
+}  // namespace cfd

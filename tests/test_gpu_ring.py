@@ -1,0 +1,143 @@
+"""The site-ring step kernel (step_ring.cuh): producer warp + TMA-fed shared-memory rings.
+
+A strip of four lattice lines marches along x; every gathered operand is read from shared
+memory (x / y neighbours from neighbouring ring slots, z neighbours and matrix values from
+the column's stage).  Each row still meets its entries in CSR order with the reference's
+roundings, so apply_filter (filter.hpp:73-116) and spmmvm_fused / recurrence_step
+(kernels.hpp:74-145) must equal the oracle bit for bit.  Option "ring" = 2 forces the kernel
+onto small lattices; Context.ring_launches proves it ran.  Covered: the three slab patterns
+(bottom / interior / top plane), generic sites (x / y wrap, open edges), periodic z, x
+segments with aprons, shallow rings, 32- and 64-unit slabs, multi-slab widths, virtual rank
+groups (halo rows behind the z -+ 1 indices, compact and full).
+"""
+import numpy as np
+import pytest
+
+import paper_1510_04895_b200 as cf
+
+pytestmark = pytest.mark.gpu
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.fixture()
+def rctx(ctx):
+    ctx.set_option("ring", 2)
+    yield ctx
+    for k in ("ring", "ring_segx", "ring_no", "ring_nz"):
+        ctx.set_option(k, 0)
+    ctx.set_option("delayed_x", 3)
+
+
+def ti(ctx, orc, l, boundary="periodic_xy_open_z"):
+    A = cf.SparseMatrix.topological_insulator(
+        ctx, cf.LatticeSpec(*l, disorder=0.5, seed=1, boundary=boundary))
+    return A, orc.topological_insulator(*l, disorder=0.5, seed=1, boundary=boundary)
+
+
+def block(A, host):
+    return cf.BlockVector(A, host.shape[1]).upload(host)
+
+
+@pytest.mark.parametrize("l,nb,boundary", [
+    ((8, 8, 5), 64, "periodic_xy_open_z"),
+    ((8, 8, 5), 32, "periodic_xy_open_z"),
+    ((7, 4, 3), 64, "periodic_xy_open_z"),
+    ((8, 12, 4), 32, "periodic_all"),
+    ((6, 8, 4), 64, "open_all"),
+    ((8, 8, 3), 96, "periodic_xy_open_z"),    # three 32-unit slabs (row copies, not site copies)
+    ((8, 4, 3), 128, "periodic_xy_open_z"),   # two 64-unit slabs
+])
+def test_ring_filter_bitexact(rctx, orc, l, nb, boundary):
+    A, c = ti(rctx, orc, l, boundary)
+    x0 = orc.randomize(c.dim, nb, 5, True)
+    p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 17, "lanczos2")
+    xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
+    X = block(A, x0)
+    before = rctx.ring_launches
+    cf.apply_filter(A, X, p)
+    assert rctx.ring_launches > before
+    assert bits_equal(X.to_numpy(), xr)
+
+
+@pytest.mark.parametrize("segx,no,nz", [(3, 4, 2), (1, 5, 3), (5, 6, 3), (64, 4, 2)])
+def test_ring_segments_and_depths(rctx, orc, segx, no, nz):
+    """x segments shorter than a line (apron columns on both sides, ragged last segment) and
+    the shallowest / deepest rings give the same bits."""
+    l, nb = (8, 8, 4), 64
+    rctx.set_option("ring_segx", segx)
+    rctx.set_option("ring_no", no)
+    rctx.set_option("ring_nz", nz)
+    A, c = ti(rctx, orc, l)
+    x0 = orc.randomize(c.dim, nb, 6, True)
+    p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 11, "jackson")
+    xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
+    X = block(A, x0)
+    before = rctx.ring_launches
+    cf.apply_filter(A, X, p)
+    assert rctx.ring_launches > before
+    assert bits_equal(X.to_numpy(), xr)
+
+
+@pytest.mark.parametrize("delayed", [0, 2, 3])
+def test_ring_step_kinds(rctx, orc, delayed):
+    """Every dot-free kind of the fused loop: kStepFused (delayed_x off), kStepRecur +
+    kStepFusedX2 / X3, and the public single steps."""
+    l, nb = (8, 8, 4), 32
+    A, c = ti(rctx, orc, l)
+    rctx.set_option("delayed_x", delayed)
+    x0 = orc.randomize(c.dim, nb, 7, True)
+    for deg in (9, 10, 11):
+        p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), deg, "lanczos2")
+        xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
+        X = block(A, x0)
+        before = rctx.ring_launches
+        cf.apply_filter(A, X, p)
+        assert rctx.ring_launches > before
+        assert bits_equal(X.to_numpy(), xr), deg
+    u, w, xx = (orc.randomize(c.dim, nb, s, True) for s in (1, 2, 3))
+    U, W, X = block(A, u), block(A, w), block(A, xx)
+    before = rctx.ring_launches
+    cf.spmmvm_fused(A, U, W, X, 0.37, -0.21, 0.83, dots=False)
+    orc.spmmvm_fused(c, u, w, xx, 0.37, -0.21, 0.83, want_dots=False)
+    assert rctx.ring_launches > before
+    assert bits_equal(W.to_numpy(), w)
+    assert bits_equal(X.to_numpy(), xx)
+    u, w = (orc.randomize(c.dim, nb, s, True) for s in (4, 5))
+    U, W = block(A, u), block(A, w)
+    cf.recurrence_step(A, U, W, 0.6, 0.1)
+    orc.recurrence_step(c, u, w, 0.6, 0.1)
+    assert bits_equal(W.to_numpy(), w)
+
+
+@pytest.mark.parametrize("world,compact", [(2, 1), (3, 1), (2, 0)])
+def test_ring_virtual_ranks(orc, world, compact):
+    """Rank partitions by z-planes: the z -+ 1 indices of a rank's outer planes point into its
+    halo regions (compact halos renumber them); interior / boundary launches of whole
+    planes."""
+    l, nb = (8, 8, 6), 64
+    spec = cf.LatticeSpec(*l, disorder=0.5, seed=2)
+    csr = orc.topological_insulator(*l, disorder=0.5, seed=2)
+    x0 = orc.randomize(csr.dim, nb, 5, True)
+    p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 14, "lanczos2")
+    xr, _ = orc.apply_filter(csr, x0, p.combined, p.alpha, p.beta)
+    g = cf.VirtualGroup(world)
+    try:
+        g.set_option("compact_halo", compact)
+        g.set_option("ring", 2)
+        As = g.topological_insulator(spec)
+        rows, a = [], 0
+        for A in As:
+            rows.append((a, a + A.local_rows))
+            a += A.local_rows
+        Xs = [cf.BlockVector(A, nb).upload(x0[a:b]) for A, (a, b) in zip(As, rows)]
+        before = sum(c.ring_launches for c in g.ranks)
+        g.apply_filter(As, Xs, p)
+        assert sum(c.ring_launches for c in g.ranks) > before
+        assert bits_equal(np.concatenate([X.to_numpy() for X in Xs]), xr)
+    finally:
+        g.close()
