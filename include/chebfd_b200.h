@@ -108,7 +108,8 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_DELAYED_X = 15, CHEBFD_OPT_BAND_BYTES = 16, CHEBFD_OPT_ASYNC_START = 17,
        CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19, CHEBFD_OPT_GRAM = 20,
        CHEBFD_OPT_GROUPED = 21, CHEBFD_OPT_GROUP_LINES = 22, CHEBFD_OPT_RING = 23,
-       CHEBFD_OPT_RING_SEGX = 24, CHEBFD_OPT_RING_NO = 25, CHEBFD_OPT_RING_NZ = 26 };
+       CHEBFD_OPT_RING_SEGX = 24, CHEBFD_OPT_RING_NO = 25, CHEBFD_OPT_RING_NZ = 26,
+       CHEBFD_OPT_RING_ROWS = 27, CHEBFD_OPT_RING_CONSTS = 28 };
 /* CHEBFD_OPT_RING: the site-ring step kernel (csrc/step_ring.cuh) on complex TI lattice
  * operators with blocks of a multiple of 32 columns: a producer warp stages each x-column of
  * a strip of four lattice lines (site blocks, z -+ 1 rows, matrix values) in shared-memory
@@ -117,7 +118,11 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
  * V_n-only steps; W and X bit-identical to the other step kernels.  1: the launches the
  * row-group kernel would take (band order); 2: every applicable launch; 0: off.
  * CHEBFD_OPT_RING_SEGX (x-columns per CTA, default 64), _NO / _NZ (ring depths, default
- * 5 / 3). */
+ * 5 / 3), _ROWS (rows of a site per consumer thread: 4, 2 or 1; default 2 -- 4 / rows
+ * consumer groups share a site's staged operands), _CONSTS (default 1: where every static
+ * site of a pattern holds the same off-diagonal values -- the lattice models' hopping terms
+ * -- the products take them as kernel-parameter constants and only the four diagonal values
+ * per site are read; the builder compares the stored values bit for bit). */
 /* CHEBFD_OPT_GROUPED (default 1): dot-free steps that run in the band tile order (lattice
  * operators whose z-planes exceed the L2 budget, CHEBFD_OPT_BAND_BYTES) use the row-group
  * kernel: four consecutive rows -- a lattice site's orbitals -- share one merged list of

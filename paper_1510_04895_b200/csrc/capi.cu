@@ -1073,6 +1073,10 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->ring_no = static_cast<int>(value);
         else if (option == CHEBFD_OPT_RING_NZ)
             c->ring_nz = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_ROWS)
+            c->ring_rows = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_CONSTS)
+            c->ring_consts = static_cast<int>(value);
         else if (option == CHEBFD_OPT_TILES_PER_CTA)
             c->tiles_per_cta = static_cast<int>(std::max<int64_t>(value, 0));
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)

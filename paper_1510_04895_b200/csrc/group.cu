@@ -295,6 +295,54 @@ __global__ void ring_plan_kernel(const int64_t* __restrict__ tile_cptr,
         make_int4(static_cast<int>(voff & 0xFFFFFFFFll), static_cast<int>(voff >> 32), h.w, nv);
 }
 
+
+// first static group of each pattern (reference values for the constant check)
+__global__ void ring_first_kernel(const int4* __restrict__ plan, int64_t ngroups,
+                                  unsigned long long* __restrict__ first) {
+    const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (g >= ngroups) return;
+    const int pat = plan[2 * g + 1].z;
+    if (pat >= 1 && pat <= 3) atomicMin(&first[pat - 1], static_cast<unsigned long long>(g));
+}
+
+// do all static groups of a pattern hold the reference group's values, the own-row diagonal
+// entries (k = OWN + r, row r) aside?
+template <class P>
+__device__ bool ring_same_values(const double2* v, const double2* ref) {
+    for (int k = 0; k < P::NC; ++k)
+        for (int r = 0; r < kGroupRows; ++r) {
+            if (!((P::m(k) >> r) & 1u) || k == P::OWN + r) continue;
+            const int i = P::voff(k, r);
+            if (__double_as_longlong(v[i].x) != __double_as_longlong(ref[i].x) ||
+                __double_as_longlong(v[i].y) != __double_as_longlong(ref[i].y))
+                return false;
+        }
+    return true;
+}
+
+__global__ void ring_const_kernel(const int4* __restrict__ plan, const double2* __restrict__ vals,
+                                  int64_t ngroups, const unsigned long long* __restrict__ first,
+                                  int* __restrict__ bad) {
+    const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (g >= ngroups) return;
+    const int4 b = plan[2 * g + 1];
+    if (b.z < 1 || b.z > 3) return;
+    const int4 rb = plan[2 * first[b.z - 1] + 1];
+    auto off = [](const int4& q) {
+        return static_cast<int64_t>(static_cast<unsigned>(q.x)) | (static_cast<int64_t>(q.y) << 32);
+    };
+    const double2* v = vals + off(b);
+    const double2* ref = vals + off(rb);
+    bool ok;
+    if (b.z == 1)
+        ok = ring_same_values<PatTiMid>(v, ref);
+    else if (b.z == 2)
+        ok = ring_same_values<PatTiLo>(v, ref);
+    else
+        ok = ring_same_values<PatTiHi>(v, ref);
+    if (!ok) atomicExch(bad, 1);
+}
+
 }  // namespace
 
 // plan of the site-ring step kernel: complex lattice operators whose rows are whole sites in
@@ -318,6 +366,35 @@ static void build_ring_plan(Matrix& m, cudaStream_t st) {
     CFD_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CFD_CUDA(cudaStreamSynchronize(st));
     gm.ring_ok = h == 0;
+    gm.ring_const_ok = false;
+    if (!gm.ring_ok) return;
+    // constant off-diagonal values per pattern?
+    DeviceBuffer first(3 * sizeof(unsigned long long));
+    CFD_CUDA(cudaMemsetAsync(first.p, 0xFF, 3 * sizeof(unsigned long long), st));
+    CFD_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    const unsigned grid = static_cast<unsigned>((ngroups + 127) / 128);
+    ring_first_kernel<<<grid, 128, 0, st>>>(gm.ring_plan.as<int4>(), ngroups,
+                                            first.as<unsigned long long>());
+    ring_const_kernel<<<grid, 128, 0, st>>>(gm.ring_plan.as<int4>(), gm.vals.as<double2>(), ngroups,
+                                            first.as<unsigned long long>(), bad.as<int>());
+    CFD_CUDA(cudaGetLastError());
+    unsigned long long hf[3];
+    CFD_CUDA(cudaMemcpyAsync(hf, first.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
+    CFD_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CFD_CUDA(cudaStreamSynchronize(st));
+    if (h != 0) return;
+    for (int q = 0; q < 3; ++q) {
+        if (hf[q] == ~0ull) continue;  // pattern absent: its constants are never used
+        int4 pb;
+        CFD_CUDA(cudaMemcpy(&pb, gm.ring_plan.as<int4>() + 2 * hf[q] + 1, sizeof(int4),
+                            cudaMemcpyDeviceToHost));
+        const int64_t voff = static_cast<int64_t>(static_cast<unsigned>(pb.x)) |
+                             (static_cast<int64_t>(pb.y) << 32);
+        const int nv = std::min(pb.w, kRingMaxVals);
+        CFD_CUDA(cudaMemcpy(gm.ring_consts[q], gm.vals.as<double2>() + voff,
+                            sizeof(double) * 2 * nv, cudaMemcpyDeviceToHost));
+    }
+    gm.ring_const_ok = true;
 }
 
 void build_grouped(Context& ctx, Matrix& m, const int64_t* d_offs, const int64_t* d_cols,

@@ -32,7 +32,7 @@ struct PatBase {
     }
 };
 struct PatTiMid : PatBase<PatTiMid> {
-    static constexpr int NC = 24, OWN = 10;
+    static constexpr int NC = 24, OWN = 10, ID = 0;
     __host__ __device__ static constexpr unsigned m(int k) {
         constexpr unsigned char t[NC] = {0x4, 0x2, 0xC, 0xC, 0x3, 0x3, 0xC, 0xC, 0x3, 0x3, 0x5, 0xA,
                                          0x5, 0xA, 0xC, 0xC, 0x3, 0x3, 0xC, 0xC, 0x3, 0x3, 0x8, 0x1};
@@ -50,7 +50,7 @@ struct PatTiMid : PatBase<PatTiMid> {
     }
 };
 struct PatTiLo : PatBase<PatTiLo> {  // no z-1 neighbours
-    static constexpr int NC = 22, OWN = 8;
+    static constexpr int NC = 22, OWN = 8, ID = 1;
     __host__ __device__ static constexpr unsigned m(int k) {
         constexpr unsigned char t[NC] = {0xC, 0xC, 0x3, 0x3, 0xC, 0xC, 0x3, 0x3, 0x5, 0xA, 0x5,
                                          0xA, 0xC, 0xC, 0x3, 0x3, 0xC, 0xC, 0x3, 0x3, 0x8, 0x1};
@@ -68,7 +68,7 @@ struct PatTiLo : PatBase<PatTiLo> {  // no z-1 neighbours
     }
 };
 struct PatTiHi : PatBase<PatTiHi> {  // no z+1 neighbours
-    static constexpr int NC = 22, OWN = 10;
+    static constexpr int NC = 22, OWN = 10, ID = 2;
     __host__ __device__ static constexpr unsigned m(int k) {
         constexpr unsigned char t[NC] = {0x4, 0x2, 0xC, 0xC, 0x3, 0x3, 0xC, 0xC, 0x3, 0x3, 0x5,
                                          0xA, 0x5, 0xA, 0xC, 0xC, 0x3, 0x3, 0xC, 0xC, 0x3, 0x3};

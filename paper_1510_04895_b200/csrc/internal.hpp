@@ -146,6 +146,12 @@ struct GroupedMatrix {
     // holds more than kRingMaxVals values.
     bool ring_ok = false;
     DeviceBuffer ring_plan;
+    // every static site of a pattern holds the same off-diagonal values (the lattice models'
+    // hopping terms): ring_consts[pattern id - 1][value index] = that value (unscaled), so
+    // the site-ring kernel multiplies with kernel-parameter constants and reads only the
+    // four diagonal (disorder) values per site from memory
+    bool ring_const_ok = false;
+    double ring_consts[3][44][2] = {};
 };
 constexpr int kRingMaxVals = 44;  // values per site staged by the site-ring kernel
 
@@ -288,6 +294,8 @@ struct Context {
     // (band-ordered launches), 2 wherever it applies; CHEBFD_OPT_RING.  ring_segx / ring_no /
     // ring_nz: x-columns per CTA and ring depths (0: defaults); CHEBFD_OPT_RING_SEGX / _NO / _NZ
     int ring = 0, ring_segx = 0, ring_no = 0, ring_nz = 0;
+    int ring_consts = 1;  // 1: constant off-diagonal values as kernel parameters where the matrix has them; CHEBFD_OPT_RING_CONSTS
+    int ring_rows = 0;  // rows of a site per consumer thread (4, 2, 1; 0: default 2); CHEBFD_OPT_RING_ROWS
     int64_t ring_launches = 0;   // step launches that ran the site-ring kernel
     // exchange only the referenced halo rows of structurally symmetric operators (lattice
     // models, bitwise-Hermitian from_csr input); CHEBFD_OPT_COMPACT_HALO

@@ -50,6 +50,13 @@ struct RingParams {
     int full;           // 1: the slab is the whole row (a site's four rows are one copy)
 };
 
+// per pattern, the (alpha-scaled) real or imaginary part of every purely real / imaginary
+// matrix value that is the same at all static sites (GroupedMatrix::ring_consts); a kernel
+// parameter, so the products take it as a constant-bank operand: no load, no register
+struct RingConsts {
+    double v[3][kRingMaxVals];
+};
+
 template <class F, int... I>
 __device__ __forceinline__ void ring_for_impl(F&& f, std::integer_sequence<int, I...>) {
     (f(std::integral_constant<int, I>{}), ...);
@@ -99,47 +106,68 @@ __device__ __forceinline__ double2 ring_operand(const RingBases& b) {
     return *reinterpret_cast<const double2*>(a);
 }
 
-template <class P, int RB>
-__device__ __forceinline__ void ring_mac(const RingBases& b, const double2* vs, double2 (&acc)[4],
-                                         double2 (&ui)[4]) {
+// products of the rows R0 .. R0 + RS - 1 of a static-pattern site: only the operands those
+// rows (or their own-row terms) need are read
+template <class P, int RB, int R0, int RS, bool CV>
+__device__ __forceinline__ void ring_mac(const RingBases& b, const double2* vs, const RingConsts& cc,
+                                         double2 (&acc)[RS], double2 (&ui)[RS]) {
     using O = Ops<true, double2>;
+    constexpr unsigned SUB = ((1u << RS) - 1u) << R0;
     ring_for<P::NC>([&](auto kt) {
         constexpr int k = decltype(kt)::value;
-        const double2 gk = ring_operand<P, k, RB>(b);
-        ring_for<kGroupRows>([&](auto rt) {
-            constexpr int r = decltype(rt)::value;
-            if constexpr ((P::m(k) >> r) & 1u) {
-                if constexpr ((P::re(k) >> r) & 1u) {
-                    const double v = vs[P::voff(k, r)].x;
-                    acc[r].x = add(acc[r].x, mul(v, gk.x));
-                    acc[r].y = add(acc[r].y, mul(v, gk.y));
-                } else if constexpr ((P::im(k) >> r) & 1u) {
-                    const double v = vs[P::voff(k, r)].y;
-                    acc[r].x = sub(acc[r].x, mul(v, gk.y));
-                    acc[r].y = add(acc[r].y, mul(v, gk.x));
-                } else {
-                    acc[r] = O::vadd(acc[r], O::prod(vs[P::voff(k, r)], gk));
+        constexpr bool own = k >= P::OWN + R0 && k < P::OWN + R0 + RS;
+        if constexpr ((P::m(k) & SUB) != 0u || own) {
+            const double2 gk = ring_operand<P, k, RB>(b);
+            ring_for<RS>([&](auto rt) {
+                constexpr int r = R0 + decltype(rt)::value;
+                constexpr int a = decltype(rt)::value;
+                if constexpr ((P::m(k) >> r) & 1u) {
+                    constexpr bool cv = CV && k != P::OWN + r;  // not the site's diagonal entry
+                    if constexpr ((P::re(k) >> r) & 1u) {
+                        double v;
+                        if constexpr (cv)
+                            v = cc.v[P::ID][P::voff(k, r)];
+                        else
+                            v = vs[P::voff(k, r)].x;
+                        acc[a].x = add(acc[a].x, mul(v, gk.x));
+                        acc[a].y = add(acc[a].y, mul(v, gk.y));
+                    } else if constexpr ((P::im(k) >> r) & 1u) {
+                        double v;
+                        if constexpr (cv)
+                            v = cc.v[P::ID][P::voff(k, r)];
+                        else
+                            v = vs[P::voff(k, r)].y;
+                        acc[a].x = sub(acc[a].x, mul(v, gk.y));
+                        acc[a].y = add(acc[a].y, mul(v, gk.x));
+                    } else {
+                        acc[a] = O::vadd(acc[a], O::prod(vs[P::voff(k, r)], gk));
+                    }
                 }
-            }
-        });
-        if constexpr (k >= P::OWN && k < P::OWN + kGroupRows) ui[k - P::OWN] = gk;
+            });
+            if constexpr (own) ui[k - P::OWN - R0] = gk;
+        }
     });
 }
 
-template <int KIND, int US>
-__global__ void __launch_bounds__(kRingSY* US + 32, 1)
-    step_ring_kernel(const StepParams p, const RingParams rp) {
+// RS rows of a site per consumer thread (4, 2 or 1): 4 / RS consumer groups share a site's
+// operands in shared memory, which multiplies the resident consumer warps -- the FP64
+// chains of 8 warps per SM do not fill the issue slots (ncu: issue 35 % busy, stalls on
+// fixed-latency dependencies)
+template <int KIND, int US, int RS, bool CV>
+__global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 32 && RS >= 2) ? 2 : 1)
+    step_ring_kernel(const StepParams p, const RingParams rp, const __grid_constant__ RingConsts cc) {
     using T = double2;
     using O = Ops<true, double2>;
     using M = double2;
     constexpr int SY = kRingSY;
     constexpr int G = kGroupRows;
+    constexpr int NG = G / RS;                      // consumer groups
     constexpr int RB = US * 16;                     // bytes of a row (slab)
     constexpr int OS = (SY + 2) * G * RB;           // own-plane column slot
     constexpr int VB = kRingMaxVals * 16;           // value bytes per site
     constexpr int ZS = SY * G * RB + SY * VB;       // z-row + value stage
-    constexpr int NCT = SY * US;                    // consumer threads
-    constexpr int NCW = NCT / 32;
+    constexpr int NCT = SY * US;                    // consumer threads per group
+    constexpr int NCW = NG * NCT / 32;              // consumer warps
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[4 * kRingMaxDepth];
     uint64_t* full_o = bars;
@@ -184,7 +212,7 @@ __global__ void __launch_bounds__(kRingSY* US + 32, 1)
             mbar_init(&empty_o[i], NCW);
         }
         for (int i = 0; i < nz; ++i) {
-            mbar_init(&full_z[i], 1);
+            mbar_init(&full_z[i], 2);  // one arrival per producer warp
             mbar_init(&empty_z[i], NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -193,82 +221,127 @@ __global__ void __launch_bounds__(kRingSY* US + 32, 1)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int pitch = p.pitch;
 
-    if (t >= NCT) {
-        // ================================ producer warp ================================
-        const int lane = t - NCT;
+    if (t >= NG * NCT) {
+        // ============================== producer warps ===============================
+        // Two warps, because issuing a bulk copy costs ~90 cycles of a warp (the lanes'
+        // operands move to uniform registers one copy at a time): warp A feeds the
+        // own-plane ring and the sites' matrix values, warp B the z -+ 1 rows.
+        const int pw = (t - NG * NCT) >> 5;
+        const int lane = t & 31;
         const T* inb = static_cast<const T*>(p.in) + p.u_off;
-        const M* gvals = static_cast<const M*>(rp.vals);
         const uint64_t pol_keep = l2_make_policy(1);
-        const uint64_t pol_stream = l2_make_policy(2);
         const int K = jhi - jlo;
-        for (int k = 0; k <= K; ++k) {
-            if (k < K) {
-                const int j = jlo + k, slot = k % no;
-                if (k >= no) mbar_wait(&empty_o[slot], ((k / no) - 1) & 1);
-                const bool apron = j < xa || j >= xb;
-                int ss, rr;
-                unsigned bytes;
-                bool active;
-                if (rp.full) {
-                    ss = lane;
-                    rr = 0;
-                    bytes = G * RB;
-                    active = lane < SY + 2;
-                } else {
-                    ss = lane >> 2;
-                    rr = lane & 3;
-                    bytes = RB;
-                    active = lane < G * (SY + 2);
-                }
+        if (pw == 0) {
+            const M* gvals = static_cast<const M*>(rp.vals);
+            const uint64_t pol_stream = l2_make_policy(2);
+            // own-plane copies of this lane: site slot ss (row rr of it unless whole sites)
+            int ss, rr;
+            unsigned obytes;
+            bool oact;
+            if (rp.full) {
+                ss = lane;
+                rr = 0;
+                obytes = G * RB;
+                oact = lane < SY + 2;
+            } else {
+                ss = lane >> 2;
+                rr = lane & 3;
+                obytes = RB;
+                oact = lane < G * (SY + 2);
+            }
+            {
                 const int y = y0 + ss - 1;
-                active = active && y >= 0 && y < ly && (!apron || (ss >= 1 && ss <= SY));
-                const unsigned total = __reduce_add_sync(0xffffffffu, active ? bytes : 0u);
-                if (lane == 0) mbar_arrive_expect_tx(&full_o[slot], total);
-                __syncwarp();
-                if (active) {
-                    const int64_t erow =
-                        p.halo_lo + G * (site0 + static_cast<int64_t>(ss - 1) * lx + j) + rr;
-                    tma_load_1d_hint(oring + static_cast<size_t>(slot) * OS + (ss * G + rr) * RB,
-                                     inb + erow * pitch, bytes, &full_o[slot], pol_keep);
+                oact = oact && y >= 0 && y < ly;
+            }
+            const bool oin = ss >= 1 && ss <= SY;  // a strip line (aprons copy only these)
+            const int64_t erow0 = p.halo_lo + G * (site0 + static_cast<int64_t>(ss - 1) * lx) + rr;
+            unsigned char* odst0 = oring + (ss * G + rr) * RB;
+            int oslot = 0, opar = 1;  // empty-barrier parity of the slot's previous use
+            int zslot = 0, zpar = 1;
+            for (int k = 0; k <= K; ++k) {
+                if (k < K) {
+                    const int j = jlo + k;
+                    if (k >= no) mbar_wait(&empty_o[oslot], opar);
+                    const bool act = oact && ((j >= xa && j < xb) || oin);
+                    const unsigned total = __reduce_add_sync(0xffffffffu, act ? obytes : 0u);
+                    if (lane == 0) mbar_arrive_expect_tx(&full_o[oslot], total);
+                    __syncwarp();
+                    if (act)
+                        tma_load_1d_hint(odst0 + static_cast<size_t>(oslot) * OS,
+                                         inb + (erow0 + static_cast<int64_t>(G) * j) * pitch, obytes,
+                                         &full_o[oslot], pol_keep);
+                    if (++oslot == no) {
+                        oslot = 0;
+                        opar ^= 1;
+                    }
+                }
+                const int c = jlo + k - 1;
+                if (c >= xa && c < xb) {  // the column's matrix values (one copy per site)
+                    const int kz = c - xa;
+                    if (kz >= nz) mbar_wait(&empty_z[zslot], zpar);
+                    unsigned bytes = 0;
+                    const void* src = nullptr;
+                    unsigned char* dst = zring + static_cast<size_t>(zslot) * ZS + SY * G * RB + lane * VB;
+                    if (lane < SY) {
+                        const int4 b = plan_s[(lane * segx + kz) * 2 + 1];
+                        const int64_t voff = static_cast<int64_t>(static_cast<unsigned>(b.x)) |
+                                             (static_cast<int64_t>(b.y) << 32);
+                        // constants cover the static sites' off-diagonal values: their four
+                        // diagonal entries sit inside the first (OWN + 4) columns' values
+                        bytes = static_cast<unsigned>(b.w) * 16u;
+                        src = gvals + voff;
+                    }
+                    const unsigned total = __reduce_add_sync(0xffffffffu, bytes);
+                    if (lane == 0) mbar_arrive_expect_tx(&full_z[zslot], total);
+                    __syncwarp();
+                    if (bytes) tma_load_1d_hint(dst, src, bytes, &full_z[zslot], pol_stream);
+                    if (++zslot == nz) {
+                        zslot = 0;
+                        zpar ^= 1;
+                    }
                 }
             }
-            const int c = jlo + k - 1;
-            if (c >= xa && c < xb) {
-                const int kz = c - xa, slot = kz % nz;
-                if (kz >= nz) mbar_wait(&empty_z[slot], ((kz / nz) - 1) & 1);
+        } else {
+            int zslot = 0, zpar = 1;
+            for (int c = xa; c < xb; ++c) {
+                const int kz = c - xa;
+                if (kz >= nz) mbar_wait(&empty_z[zslot], zpar);
                 unsigned bytes = 0;
                 const void* src = nullptr;
-                unsigned char* dst = zring + static_cast<size_t>(slot) * ZS;
-                bool keep = true;
+                unsigned char* dst = zring + static_cast<size_t>(zslot) * ZS;
                 if (lane < G * SY) {
                     const int l = lane >> 2, w = lane & 3;
                     const int4 a = plan_s[(l * segx + kz) * 2];
                     const int4 b = plan_s[(l * segx + kz) * 2 + 1];
                     const int row = w == 0 ? a.x : (w == 1 ? a.y : (w == 2 ? a.z : a.w));
+                    const int prev = w == 1 ? a.x : (w == 3 ? a.z : -2);   // the pair's first row
+                    const int next = w == 0 ? a.y : (w == 2 ? a.w : -2);   // the pair's second row
                     if (b.z != 0 && row >= 0) {
-                        bytes = RB;
-                        src = inb + static_cast<int64_t>(row) * pitch;
-                        dst += (l * G + w) * RB;
+                        // adjacent rows of a pair (whole-row slabs) travel as one copy
+                        const bool merged_away = rp.full && prev >= 0 && row == prev + 1;
+                        const bool merges = rp.full && next == row + 1;
+                        if (!merged_away) {
+                            bytes = merges ? 2 * RB : RB;
+                            src = inb + static_cast<int64_t>(row) * pitch;
+                            dst += (l * G + w) * RB;
+                        }
                     }
-                } else if (lane < (G + 1) * SY) {
-                    const int l = lane - G * SY;
-                    const int4 b = plan_s[(l * segx + kz) * 2 + 1];
-                    const int64_t voff = static_cast<int64_t>(static_cast<unsigned>(b.x)) |
-                                         (static_cast<int64_t>(b.y) << 32);
-                    bytes = static_cast<unsigned>(b.w) * 16u;
-                    src = gvals + voff;
-                    dst += SY * G * RB + l * VB;
-                    keep = false;
                 }
                 const unsigned total = __reduce_add_sync(0xffffffffu, bytes);
-                if (lane == 0) mbar_arrive_expect_tx(&full_z[slot], total);
+                if (lane == 0) mbar_arrive_expect_tx(&full_z[zslot], total);
                 __syncwarp();
-                if (bytes) tma_load_1d_hint(dst, src, bytes, &full_z[slot], keep ? pol_keep : pol_stream);
+                if (bytes) tma_load_1d_hint(dst, src, bytes, &full_z[zslot], pol_keep);
+                if (++zslot == nz) {
+                    zslot = 0;
+                    zpar ^= 1;
+                }
             }
         }
     } else {
         // ================================ consumer warps ================================
-        const int l = t / US, u = t - l * US;
+        const int grp = t / NCT;
+        const int tt = t - grp * NCT;
+        const int l = tt / US, u = tt - l * US;
         const int cu = p.u_off + u;
         const bool lane0 = (t & 31) == 0;
         const T* __restrict__ inu = static_cast<const T*>(p.in) + cu;
@@ -279,84 +352,141 @@ __global__ void __launch_bounds__(kRingSY* US + 32, 1)
         if ((KIND == kStepFusedX2 || KIND == kStepFusedX3) && p.coeff_dev) c1 = p.coeff_dev[p.coeff_index - 1];
         if (KIND == kStepFusedX3 && p.coeff_dev) c2 = p.coeff_dev[p.coeff_index - 2];
         const uint64_t pol_stream = l2_make_policy(2);
-        double dummy_a[1] = {0.0}, dummy_c[1] = {0.0};
-        int kw = 0;  // own-plane columns waited for so far
-        for (int c = xa; c < xb; ++c) {
-            const int kz = c - xa;
-            const int64_t rg = G * (site0 + static_cast<int64_t>(l) * lx + c);
-            // own-row streams first: their latency overlaps the barrier waits
-            T wi[G], xi[G];
-            int64_t own[G];
-#pragma unroll
-            for (int r = 0; r < G; ++r) {
-                own[r] = (rg + r) * pitch;
-                wi[r] = xi[r] = T{};
-                if constexpr (kind_reads_w(KIND)) wi[r] = lds_pol(&W[own[r]], pol_stream);
-                if constexpr (kind_reads_x(KIND)) xi[r] = lds_pol(&X[own[r]], pol_stream);
+
+        auto consume = [&](auto r0_tag) {
+            constexpr int R0 = decltype(r0_tag)::value;
+            double dummy_a[1] = {0.0}, dummy_c[1] = {0.0};
+            // ring positions, advanced per column (no divisions in the loop)
+            int so_m = no - 1, so_c = 0, so_p = 1 % no;    // slots of columns c - 1, c, c + 1
+            if (xa > jlo) {
+                so_m = 0;
+                so_c = 1 % no;
+                so_p = 2 % no;
             }
-            const int need = min(c + 1, jhi - 1) - jlo;
-            while (kw <= need) {
-                mbar_wait(&full_o[kw % no], (kw / no) & 1);
-                ++kw;
-            }
-            mbar_wait(&full_z[kz % nz], (kz / nz) & 1);
-            const int4 pb = plan_s[(l * segx + kz) * 2 + 1];
-            const unsigned char* oc = oring + static_cast<size_t>((c - jlo) % no) * OS + u * 16;
-            const unsigned char* om = oring + static_cast<size_t>((c - 1 - jlo + no) % no) * OS + u * 16;
-            const unsigned char* op = oring + static_cast<size_t>((c + 1 - jlo) % no) * OS + u * 16;
-            const unsigned char* zb = zring + static_cast<size_t>(kz % nz) * ZS;
-            const M* vs = reinterpret_cast<const M*>(zb + SY * G * RB + l * VB);
-            RingBases b;
-            b.ym = oc + l * (G * RB);
-            b.own = oc + (l + 1) * (G * RB);
-            b.yp = oc + (l + 2) * (G * RB);
-            b.xm = om + (l + 1) * (G * RB);
-            b.xp = op + (l + 1) * (G * RB);
-            b.zlo = zb + l * (G * RB) + u * 16;
-            b.zhi = b.zlo + 2 * RB;
-            T acc[G], ui[G];
+            int wslot = 0, wpar = 0, kw = 0;  // next own-plane column to wait for
+            int zslot = 0, zpar = 0;
+            const int64_t rg0 = G * (site0 + static_cast<int64_t>(l) * lx) + R0;
+            auto load_rows = [&](int c, T (&wv)[RS], T (&xv)[RS]) {
 #pragma unroll
-            for (int r = 0; r < G; ++r) acc[r] = O::zero();
-            const int pat = pb.z;
-            if (pat == 1) {
-                ring_mac<PatTiMid, RB>(b, vs, acc, ui);
-            } else if (pat == 2) {
-                ring_mac<PatTiLo, RB>(b, vs, acc, ui);
-            } else if (pat == 3) {
-                ring_mac<PatTiHi, RB>(b, vs, acc, ui);
-            } else {
-                // generic site (x / y wrap, open edges): merged columns gathered from global
-                const int4 pa = plan_s[(l * segx + kz) * 2];
-                const int64_t coff = static_cast<int64_t>(static_cast<unsigned>(pa.x)) |
-                                     (static_cast<int64_t>(pa.y) << 32);
-                const int* cl = rp.cols + coff;
-                const int n = pa.z;
-                int vi = 0;
+                for (int r = 0; r < RS; ++r) {
+                    const int64_t own = (rg0 + static_cast<int64_t>(G) * c + r) * pitch;
+                    wv[r] = xv[r] = T{};
+                    if constexpr (kind_reads_w(KIND)) wv[r] = lds_pol(&W[own], pol_stream);
+                    if constexpr (kind_reads_x(KIND)) xv[r] = lds_pol(&X[own], pol_stream);
+                }
+            };
+            T wi[RS], xi[RS];
+            load_rows(xa, wi, xi);
+            for (int c = xa; c < xb; ++c) {
+                const int kz = c - xa;
+                // next column's own-row streams: a step of latency hiding in registers
+                T wn[RS], xn[RS];
+#pragma unroll
+                for (int r = 0; r < RS; ++r) wn[r] = xn[r] = T{};
+                if (c + 1 < xb) load_rows(c + 1, wn, xn);
+                const int need = min(c + 1, jhi - 1) - jlo;
+                while (kw <= need) {
+                    mbar_wait(&full_o[wslot], wpar);
+                    ++kw;
+                    if (++wslot == no) {
+                        wslot = 0;
+                        wpar ^= 1;
+                    }
+                }
+                mbar_wait(&full_z[zslot], zpar);
+                const int4 pb = plan_s[(l * segx + kz) * 2 + 1];
+                const unsigned char* oc = oring + static_cast<size_t>(so_c) * OS + u * 16;
+                const unsigned char* om = oring + static_cast<size_t>(so_m) * OS + u * 16;
+                const unsigned char* op = oring + static_cast<size_t>(so_p) * OS + u * 16;
+                const unsigned char* zb = zring + static_cast<size_t>(zslot) * ZS;
+                const M* vs = reinterpret_cast<const M*>(zb + SY * G * RB + l * VB);
+                RingBases b;
+                b.ym = oc + l * (G * RB);
+                b.own = oc + (l + 1) * (G * RB);
+                b.yp = oc + (l + 2) * (G * RB);
+                b.xm = om + (l + 1) * (G * RB);
+                b.xp = op + (l + 1) * (G * RB);
+                b.zlo = zb + l * (G * RB) + u * 16;
+                b.zhi = b.zlo + 2 * RB;
+                T acc[RS], ui[RS];
+#pragma unroll
+                for (int r = 0; r < RS; ++r) acc[r] = O::zero();
+                const int pat = pb.z;
+                if (pat == 1) {
+                    ring_mac<PatTiMid, RB, R0, RS, CV>(b, vs, cc, acc, ui);
+                } else if (pat == 2) {
+                    ring_mac<PatTiLo, RB, R0, RS, CV>(b, vs, cc, acc, ui);
+                } else if (pat == 3) {
+                    ring_mac<PatTiHi, RB, R0, RS, CV>(b, vs, cc, acc, ui);
+                } else {
+                    // generic site (x / y wrap, open edges): merged columns gathered from
+                    // global memory; a column's values follow its set rows in increasing order
+                    const int4 pa = plan_s[(l * segx + kz) * 2];
+                    const int64_t coff = static_cast<int64_t>(static_cast<unsigned>(pa.x)) |
+                                         (static_cast<int64_t>(pa.y) << 32);
+                    const int* cl = rp.cols + coff;
+                    const int n = pa.z;
+                    constexpr unsigned SUB = ((1u << RS) - 1u) << R0;
+                    int vi = 0;
 #pragma unroll 4
-                for (int k = 0; k < n; ++k) {
-                    const unsigned cw = static_cast<unsigned>(__ldg(cl + k));
-                    const unsigned m = cw >> 28;
-                    const T g = ldg(&inu[static_cast<int64_t>(cw & 0x0FFFFFFFu) * pitch]);
+                    for (int k = 0; k < n; ++k) {
+                        const unsigned cw = static_cast<unsigned>(__ldg(cl + k));
+                        const unsigned m = cw >> 28;
+                        if (m & SUB) {
+                            const T g = ldg(&inu[static_cast<int64_t>(cw & 0x0FFFFFFFu) * pitch]);
 #pragma unroll
-                    for (int r = 0; r < G; ++r)
-                        if (m & (1u << r)) {
-                            acc[r] = O::vadd(acc[r], O::prod(vs[vi], g));
-                            ++vi;
+                            for (int r = 0; r < RS; ++r)
+                                if (m & (1u << (R0 + r)))
+                                    acc[r] = O::vadd(
+                                        acc[r], O::prod(vs[vi + __popc(m & ((1u << (R0 + r)) - 1u))], g));
                         }
+                        vi += __popc(m);
+                    }
+#pragma unroll
+                    for (int r = 0; r < RS; ++r)
+                        ui[r] = *reinterpret_cast<const T*>(b.own + (R0 + r) * RB);
                 }
 #pragma unroll
-                for (int r = 0; r < G; ++r) ui[r] = *reinterpret_cast<const T*>(b.own + r * RB);
-            }
+                for (int r = 0; r < RS; ++r)
+                    step_epilogue<O, T, KIND, 0>(acc[r], ui[r], wi[r], xi[r], T{},
+                                                 (rg0 + static_cast<int64_t>(G) * c + r) * pitch, W, X,
+                                                 static_cast<T*>(nullptr), p.beta, coeff, c1, c2,
+                                                 dummy_a, dummy_c);
+                __syncwarp();
+                if (lane0) {
+                    mbar_arrive(&empty_z[zslot]);
+                    if (c - 1 >= jlo) mbar_arrive(&empty_o[so_m]);
+                }
+                so_m = so_c;
+                so_c = so_p;
+                if (++so_p == no) so_p = 0;
+                if (++zslot == nz) {
+                    zslot = 0;
+                    zpar ^= 1;
+                }
 #pragma unroll
-            for (int r = 0; r < G; ++r)
-                step_epilogue<O, T, KIND, 0>(acc[r], ui[r], wi[r], xi[r], T{}, own[r], W, X,
-                                             static_cast<T*>(nullptr), p.beta, coeff, c1, c2,
-                                             dummy_a, dummy_c);
-            __syncwarp();
-            if (lane0) {
-                mbar_arrive(&empty_z[kz % nz]);
-                if (c - 1 >= jlo) mbar_arrive(&empty_o[(c - 1 - jlo) % no]);
+                for (int r = 0; r < RS; ++r) {
+                    wi[r] = wn[r];
+                    xi[r] = xn[r];
+                }
             }
+        };
+        if constexpr (RS == G) {
+            consume(std::integral_constant<int, 0>{});
+        } else if constexpr (RS == 2) {
+            if (grp == 0)
+                consume(std::integral_constant<int, 0>{});
+            else
+                consume(std::integral_constant<int, 2>{});
+        } else {
+            if (grp == 0)
+                consume(std::integral_constant<int, 0>{});
+            else if (grp == 1)
+                consume(std::integral_constant<int, 1>{});
+            else if (grp == 2)
+                consume(std::integral_constant<int, 2>{});
+            else
+                consume(std::integral_constant<int, 3>{});
         }
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -384,7 +514,8 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     if (ly % SY != 0 || lx < 1 || lx > (1 << 24) || ly > (1 << 24)) return false;
     const void* svals = ring_scaled_values(a, s.alpha);
     if (!svals) return false;
-    const int us = units % 64 == 0 ? 64 : 32;
+    // 64-unit slabs (one CTA per SM) unless CHEBFD_OPT_SLAB_UNITS asks for 32 (two CTAs per SM)
+    const int us = (units % 64 == 0 && ctx.slab_units != 32) ? 64 : 32;
     // default (CHEBFD_OPT_RING = 1): where the row-group kernel would run, i.e. the
     // band-ordered launches (planes beyond the L2 budget); 2: wherever it applies
     if (ctx.ring == 1) {
@@ -415,7 +546,37 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     const int64_t nseg = (lx + segx - 1) / segx;
     const int64_t grid = strips * planes * nseg;
     if (grid >= (int64_t(1) << 31)) return false;
-    auto kernel = us == 64 ? step_ring_kernel<KIND, 64> : step_ring_kernel<KIND, 32>;
+    // rows per consumer thread: 2 by default (16 consumer warps per 64-unit strip CTA)
+    int rs = ctx.ring_rows > 0 ? ctx.ring_rows : 2;
+    if (rs != 4 && rs != 2 && rs != 1) rs = 2;
+    if (us == 64 && rs == 1) rs = 2;  // 1024 consumer threads + the producer warp do not fit
+    // constant off-diagonal values (kernel parameters) where the matrix has them
+    const bool cv = gm.ring_const_ok && ctx.ring_consts != 0;
+    if (!cv) rs = 2;
+    if (us == 32 && rs == 4) rs = 2;
+    void (*kernel)(const StepParams, const RingParams, const RingConsts) =
+        !cv ? (us == 64 ? step_ring_kernel<KIND, 64, 2, false> : step_ring_kernel<KIND, 32, 2, false>)
+        : us == 64 ? (rs == 4 ? step_ring_kernel<KIND, 64, 4, true> : step_ring_kernel<KIND, 64, 2, true>)
+                   : (rs == 2 ? step_ring_kernel<KIND, 32, 2, true> : step_ring_kernel<KIND, 32, 1, true>);
+    RingConsts cc{};
+    if (cv) {
+        // the value a product uses: the real or the imaginary part, scaled as the grouped
+        // value copies are (one IEEE multiply per component, group.cu scale_kernel)
+        auto fill = [&](auto pat) {
+            using P = decltype(pat);
+            for (int k = 0; k < P::NC; ++k)
+                for (int r = 0; r < kGroupRows; ++r) {
+                    if (!((P::m(k) >> r) & 1u)) continue;
+                    const int i = P::voff(k, r);
+                    const double* v = gm.ring_consts[P::ID][i];
+                    volatile double prod = ((P::im(k) >> r) & 1u) ? v[1] * s.alpha : v[0] * s.alpha;
+                    cc.v[P::ID][i] = s.alpha == 1.0 ? (((P::im(k) >> r) & 1u) ? v[1] : v[0]) : prod;
+                }
+        };
+        fill(PatTiMid{});
+        fill(PatTiLo{});
+        fill(PatTiHi{});
+    }
     static thread_local std::map<std::pair<const void*, int>, size_t> attr_set;
     auto& cur = attr_set[std::make_pair(reinterpret_cast<const void*>(kernel), ctx.device)];
     if (cur < smem) {
@@ -458,7 +619,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         const bool pdl = s.pdl_ok && ctx.pdl == 2;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(grid));
-        cfg.blockDim = dim3(static_cast<unsigned>(SY * us + 32));
+        cfg.blockDim = dim3(static_cast<unsigned>((kGroupRows / rs) * SY * us + 64));
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
@@ -466,7 +627,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        CFD_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, rp));
+        CFD_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, rp, cc));
         CFD_CUDA(cudaGetLastError());
         ctx.launches++;
         ctx.ring_launches++;

@@ -28,8 +28,9 @@ def bits_equal(a, b):
 def rctx(ctx):
     ctx.set_option("ring", 2)
     yield ctx
-    for k in ("ring", "ring_segx", "ring_no", "ring_nz"):
+    for k in ("ring", "ring_segx", "ring_no", "ring_nz", "ring_rows"):
         ctx.set_option(k, 0)
+    ctx.set_option("ring_consts", 1)
     ctx.set_option("delayed_x", 3)
 
 
@@ -75,6 +76,29 @@ def test_ring_segments_and_depths(rctx, orc, segx, no, nz):
     A, c = ti(rctx, orc, l)
     x0 = orc.randomize(c.dim, nb, 6, True)
     p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 11, "jackson")
+    xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
+    X = block(A, x0)
+    before = rctx.ring_launches
+    cf.apply_filter(A, X, p)
+    assert rctx.ring_launches > before
+    assert bits_equal(X.to_numpy(), xr)
+
+
+@pytest.mark.parametrize("consts", [1, 0])
+@pytest.mark.parametrize("rows", [4, 2, 1])
+@pytest.mark.parametrize("l,nb,boundary", [((8, 8, 4), 64, "periodic_xy_open_z"),
+                                           ((8, 8, 4), 32, "periodic_all"),
+                                           ((6, 4, 3), 32, "open_all")])
+def test_ring_rows_per_thread(rctx, orc, rows, l, nb, boundary, consts):
+    """4, 2 or 1 rows of a site per consumer thread (1, 2 or 4 consumer groups sharing the
+    staged operands; 64-unit slabs run at most 2 groups): static and generic sites.  With
+    and without the hopping values as kernel-parameter constants (the builder found every
+    static site of a pattern to hold the same off-diagonal values)."""
+    rctx.set_option("ring_rows", rows)
+    rctx.set_option("ring_consts", consts)
+    A, c = ti(rctx, orc, l, boundary)
+    x0 = orc.randomize(c.dim, nb, 8, True)
+    p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 13, "lanczos2")
     xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
     X = block(A, x0)
     before = rctx.ring_launches

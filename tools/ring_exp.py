@@ -43,10 +43,12 @@ def main():
         b_fused = nnz * 20 + 5 * D * nb * 16
         for s in args.sets.split(";"):
             opts = dict(kv.split("=") for kv in s.split(",") if kv)
-            for k in ("ring", "ring_segx", "ring_no", "ring_nz"):
-                ctx.set_option(k, int(opts.get(k, 0)))
+            defaults = {"ring": 0, "ring_segx": 0, "ring_no": 0, "ring_nz": 0, "ring_rows": 0,
+                        "ring_consts": 1, "slab_units": 0, "band_bytes": 16 << 20}
+            for k, d in defaults.items():
+                ctx.set_option(k, int(opts.get(k, d)))
             for k, v in opts.items():
-                if not k.startswith("ring"):
+                if k not in defaults:
                     ctx.set_option(k, int(v))
             r0, g0 = ctx.ring_launches, ctx.group_launches
             cf.apply_filter(A, X, p)
