@@ -58,7 +58,7 @@ WORKLOADS = {
     "c2": (64, 64, 64, 32, 100, False, "configs[1]"),
 }
 NCU_TRAFFIC = {  # committed ncu captures of the dominant kernel for a workload
-    "c4": "profiles/r02b_c4_recur_step.json",
+    "c4": "profiles/r02c_c4_ring_recur_step.json",
     "c2": "profiles/r02_c2_recur_step.json",
 }
 
@@ -267,12 +267,13 @@ def run_ours(args):
     ctx.synchronize()
     nrec = 20
     ctx.record(4)
-    grp0 = ctx.group_launches
+    grp0, ring0 = ctx.group_launches, ctx.ring_launches
     for _ in range(nrec):
         cf.recurrence_step(A, U, W, p.alpha, p.beta)
         U, W = W, U
     ctx.record(5)
     grouped = ctx.group_launches - grp0 >= nrec  # which step kernel the library chose
+    ringed = ctx.ring_launches - ring0 >= nrec
     rec_ms = ctx.elapsed_ms(4, 5) / nrec
     # ---- the reference's fused step itself (spmmvm_fused, kernels.hpp:74-118): W <- 2(aH+b)U - W,
     # X += c W every launch (5 block streams), 10 launches, no dots
@@ -334,7 +335,9 @@ def run_ours(args):
             "roofline": {
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": ("step_group_kernel<complex, kStepRecur> (row-group kernel, band order)"
+                "kernel": ("step_ring_kernel<kStepRecur> (site-ring kernel: producer warps + "
+                           "TMA-fed shared-memory rings)" if ringed else
+                           "step_group_kernel<complex, kStepRecur> (row-group kernel, band order)"
                            if grouped else "step_tma_kernel<complex, kStepRecur> (SELL kernel)")
                           + ": the V_n-only step, 2 of every 3 filter steps",
                 "algorithmic_bytes": rec_bytes,

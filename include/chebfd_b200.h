@@ -109,20 +109,24 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_TILES_PER_CTA = 18, CHEBFD_OPT_COMPACT_HALO = 19, CHEBFD_OPT_GRAM = 20,
        CHEBFD_OPT_GROUPED = 21, CHEBFD_OPT_GROUP_LINES = 22, CHEBFD_OPT_RING = 23,
        CHEBFD_OPT_RING_SEGX = 24, CHEBFD_OPT_RING_NO = 25, CHEBFD_OPT_RING_NZ = 26,
-       CHEBFD_OPT_RING_ROWS = 27, CHEBFD_OPT_RING_CONSTS = 28 };
+       CHEBFD_OPT_RING_ROWS = 27, CHEBFD_OPT_RING_CONSTS = 28,
+       CHEBFD_OPT_RING_TMAP = 29, CHEBFD_OPT_RING_ORDER = 30, CHEBFD_OPT_RING_UNIT = 31 };
 /* CHEBFD_OPT_RING: the site-ring step kernel (csrc/step_ring.cuh) on complex TI lattice
  * operators with blocks of a multiple of 32 columns: a producer warp stages each x-column of
  * a strip of four lattice lines (site blocks, z -+ 1 rows, matrix values) in shared-memory
  * rings by TMA bulk copies, consumer warps multiply straight from shared memory, so a site
  * block crosses L2 -> SM about once instead of once per referencing site.  Dot-free fused /
- * V_n-only steps; W and X bit-identical to the other step kernels.  1: the launches the
- * row-group kernel would take (band order); 2: every applicable launch; 0: off.
+ * V_n-only steps; W and X bit-identical to the other step kernels.  1 (default): lattices
+ * whose z-plane of the block exceeds 2 x CHEBFD_OPT_BAND_BYTES (C4: 1 GB planes); 2: every
+ * applicable launch; 0: off (the row-group / SELL kernels).
  * CHEBFD_OPT_RING_SEGX (x-columns per CTA, default 64), _NO / _NZ (ring depths, default
  * 5 / 3), _ROWS (rows of a site per consumer thread: 4, 2 or 1; default 2 -- 4 / rows
  * consumer groups share a site's staged operands), _CONSTS (default 1: where every static
  * site of a pattern holds the same off-diagonal values -- the lattice models' hopping terms
  * -- the products take them as kernel-parameter constants and only the four diagonal values
- * per site are read; the builder compares the stored values bit for bit). */
+ * per site are read; the builder compares the stored values bit for bit), _TMAP (tensor-map
+ * TMA: a site's four rows / a z -+ 1 row pair of a column slab as one 2D box copy; 1 =
+ * for slabs narrower than the row (default), 2 = always, 0 = per-row 1D bulk copies). */
 /* CHEBFD_OPT_GROUPED (default 1): dot-free steps that run in the band tile order (lattice
  * operators whose z-planes exceed the L2 budget, CHEBFD_OPT_BAND_BYTES) use the row-group
  * kernel: four consecutive rows -- a lattice site's orbitals -- share one merged list of

@@ -194,7 +194,8 @@ class Context:
                 "band_bytes": 16, "async_start": 17, "tiles_per_cta": 18,
                 "compact_halo": 19, "gram": 20, "grouped": 21, "group_lines": 22,
                 "ring": 23, "ring_segx": 24, "ring_no": 25, "ring_nz": 26,
-                "ring_rows": 27, "ring_consts": 28}[name]
+                "ring_rows": 27, "ring_consts": 28, "ring_tmap": 29,
+                "ring_order": 30, "ring_unit": 31}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):

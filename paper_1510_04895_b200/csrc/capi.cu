@@ -1077,6 +1077,12 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->ring_rows = static_cast<int>(value);
         else if (option == CHEBFD_OPT_RING_CONSTS)
             c->ring_consts = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_TMAP)
+            c->ring_tmap = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_ORDER)
+            c->ring_order = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_UNIT)
+            c->ring_spb_ctas = static_cast<int>(value);
         else if (option == CHEBFD_OPT_TILES_PER_CTA)
             c->tiles_per_cta = static_cast<int>(std::max<int64_t>(value, 0));
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)

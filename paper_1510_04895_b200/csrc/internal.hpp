@@ -290,10 +290,13 @@ struct Context {
     int group_lines = 1;  // lattice lines per tile of the grouped form (1: linear); set before
                           // building matrices (CHEBFD_OPT_GROUP_LINES)
     int64_t group_launches = 0;  // step launches that ran the row-group kernel
-    // site-ring step kernel (step_ring.cuh): 0 off, 1 where the row-group kernel would run
-    // (band-ordered launches), 2 wherever it applies; CHEBFD_OPT_RING.  ring_segx / ring_no /
+    // site-ring step kernel (step_ring.cuh): 0 off, 1 (default) on lattices whose z-plane of
+    // the block exceeds 2 x band_bytes, 2 wherever it applies; CHEBFD_OPT_RING.  ring_segx / ring_no /
     // ring_nz: x-columns per CTA and ring depths (0: defaults); CHEBFD_OPT_RING_SEGX / _NO / _NZ
-    int ring = 0, ring_segx = 0, ring_no = 0, ring_nz = 0;
+    int ring = 1, ring_segx = 0, ring_no = 0, ring_nz = 0;
+    int ring_order = 0;   // CTA order: 0 x segments fastest (bands of band_bytes), 1 x segments slowest; CHEBFD_OPT_RING_ORDER
+    int ring_spb_ctas = 0;  // order 1: CTAs per (segment, band) unit (0: the SM count); CHEBFD_OPT_RING_UNIT
+    int ring_tmap = 1;    // tensor-map TMA copies: 1 for column slabs, 2 always, 0 never; CHEBFD_OPT_RING_TMAP
     int ring_consts = 1;  // 1: constant off-diagonal values as kernel parameters where the matrix has them; CHEBFD_OPT_RING_CONSTS
     int ring_rows = 0;  // rows of a site per consumer thread (4, 2, 1; 0: default 2); CHEBFD_OPT_RING_ROWS
     int64_t ring_launches = 0;   // step launches that ran the site-ring kernel

@@ -27,6 +27,8 @@
 // rank boundaries need nothing special), the site's value offset and pattern id.  x / y
 // neighbours of static sites are checked there to be the lattice neighbours.
 #pragma once
+#include <cuda.h>
+
 #include <utility>
 
 #include "group_patterns.hpp"
@@ -46,8 +48,10 @@ struct RingParams {
     int planes;         // planes of this launch
     int segx, nseg;     // x-columns per CTA, segments per line
     int spb;            // strips per band (band order of the grid)
+    int nbands, order;  // bands per plane; 0: x segments fastest, 1: x segments slowest
     int no, nz;         // ring depths: own-plane columns, z / value stages
-    int full;           // 1: the slab is the whole row (a site's four rows are one copy)
+    int full;           // 1: the slab is the whole row (a site's four rows are one 1D copy)
+    int tmap;           // 1: tensor-map copies (RingMaps): whole sites / row pairs for any slab
 };
 
 // per pattern, the (alpha-scaled) real or imaginary part of every purely real / imaginary
@@ -74,6 +78,55 @@ __device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uns
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+// Tensor-map TMA (cp.async.bulk.tensor.2d, UTMALDG): the gathered block as a 2D tensor
+// [extended rows][doubles of a row]; a box is R rows x one slab of columns, so a site's four
+// rows (or a z -+ 1 row pair) of any column slab travel as ONE copy whatever the row pitch.
+struct RingMaps {
+    CUtensorMap m4, m2, m1;  // boxes of 4, 2 and 1 rows
+};
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* tm, int c0, int c1,
+                                                 uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+using TensorMapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                       const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                       CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+// cuTensorMapEncodeTiled through the runtime (the library does not link libcuda); null if absent
+inline TensorMapEncodeFn tensor_map_encoder() {
+    static TensorMapEncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<TensorMapEncodeFn>(f);
+    }();
+    return fn;
+}
+// maps over the block at `base` (ext_rows rows of `pitch` 16-byte units), boxes of us units
+inline bool make_ring_maps(RingMaps& m, const void* base, int64_t ext_rows, int pitch, int us) {
+    TensorMapEncodeFn enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(pitch) * 2, static_cast<cuuint64_t>(ext_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 16};
+    const cuuint32_t estr[2] = {1, 1};
+    CUtensorMap* maps[3] = {&m.m4, &m.m2, &m.m1};
+    const cuuint32_t rows[3] = {4, 2, 1};
+    for (int i = 0; i < 3; ++i) {
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(us) * 2, rows[i]};
+        if (enc(maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -155,7 +208,8 @@ __device__ __forceinline__ void ring_mac(const RingBases& b, const double2* vs, 
 // fixed-latency dependencies)
 template <int KIND, int US, int RS, bool CV>
 __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 32 && RS >= 2) ? 2 : 1)
-    step_ring_kernel(const StepParams p, const RingParams rp, const __grid_constant__ RingConsts cc) {
+    step_ring_kernel(const StepParams p, const RingParams rp, const __grid_constant__ RingConsts cc,
+                     const __grid_constant__ RingMaps tm) {
     using T = double2;
     using O = Ops<true, double2>;
     using M = double2;
@@ -183,12 +237,25 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
     // CTA -> (band of strips, plane, strip in the band, x segment): planes innermost over a
     // band, so the z -+ 1 rows a strip reads were own rows of a CTA a band slice earlier
     unsigned idx = blockIdx.x;
-    const int q = static_cast<int>(idx % static_cast<unsigned>(rp.nseg));
-    idx /= static_cast<unsigned>(rp.nseg);
-    const int sb = static_cast<int>(idx % static_cast<unsigned>(rp.spb));
-    idx /= static_cast<unsigned>(rp.spb);
-    const int z = static_cast<int>(idx % static_cast<unsigned>(rp.planes));
-    const int band = static_cast<int>(idx / static_cast<unsigned>(rp.planes));
+    int q, sb, z, band;
+    if (rp.order == 0) {
+        q = static_cast<int>(idx % static_cast<unsigned>(rp.nseg));
+        idx /= static_cast<unsigned>(rp.nseg);
+        sb = static_cast<int>(idx % static_cast<unsigned>(rp.spb));
+        idx /= static_cast<unsigned>(rp.spb);
+        z = static_cast<int>(idx % static_cast<unsigned>(rp.planes));
+        band = static_cast<int>(idx / static_cast<unsigned>(rp.planes));
+    } else {
+        // x segment slowest: a wave of CTAs is (all planes) x (spb adjacent strips) of one x
+        // segment marching in lockstep, so the strips' y -+ 1 halo lines and z -+ 1 rows are
+        // being read by their owners at the same time (one DRAM read, L2 hits for the rest)
+        sb = static_cast<int>(idx % static_cast<unsigned>(rp.spb));
+        idx /= static_cast<unsigned>(rp.spb);
+        z = static_cast<int>(idx % static_cast<unsigned>(rp.planes));
+        idx /= static_cast<unsigned>(rp.planes);
+        band = static_cast<int>(idx % static_cast<unsigned>(rp.nbands));
+        q = static_cast<int>(idx / static_cast<unsigned>(rp.nbands));
+    }
     const int lx = rp.lx, ly = rp.ly, segx = rp.segx;
     const int y0 = (band * rp.spb + sb) * SY;
     const int xa = q * segx;
@@ -238,7 +305,7 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
             int ss, rr;
             unsigned obytes;
             bool oact;
-            if (rp.full) {
+            if (rp.full || rp.tmap) {
                 ss = lane;
                 rr = 0;
                 obytes = G * RB;
@@ -266,10 +333,16 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
                     const unsigned total = __reduce_add_sync(0xffffffffu, act ? obytes : 0u);
                     if (lane == 0) mbar_arrive_expect_tx(&full_o[oslot], total);
                     __syncwarp();
-                    if (act)
-                        tma_load_1d_hint(odst0 + static_cast<size_t>(oslot) * OS,
-                                         inb + (erow0 + static_cast<int64_t>(G) * j) * pitch, obytes,
-                                         &full_o[oslot], pol_keep);
+                    if (act) {
+                        if (rp.tmap)
+                            tma_load_2d_hint(odst0 + static_cast<size_t>(oslot) * OS, &tm.m4, p.u_off * 2,
+                                             static_cast<int>(erow0 + static_cast<int64_t>(G) * j),
+                                             &full_o[oslot], pol_keep);
+                        else
+                            tma_load_1d_hint(odst0 + static_cast<size_t>(oslot) * OS,
+                                             inb + (erow0 + static_cast<int64_t>(G) * j) * pitch, obytes,
+                                             &full_o[oslot], pol_keep);
+                    }
                     if (++oslot == no) {
                         oslot = 0;
                         opar ^= 1;
@@ -308,6 +381,7 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
                 if (kz >= nz) mbar_wait(&empty_z[zslot], zpar);
                 unsigned bytes = 0;
                 const void* src = nullptr;
+                int zrow = 0;
                 unsigned char* dst = zring + static_cast<size_t>(zslot) * ZS;
                 if (lane < G * SY) {
                     const int l = lane >> 2, w = lane & 3;
@@ -318,11 +392,13 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
                     const int next = w == 0 ? a.y : (w == 2 ? a.w : -2);   // the pair's second row
                     if (b.z != 0 && row >= 0) {
                         // adjacent rows of a pair (whole-row slabs) travel as one copy
-                        const bool merged_away = rp.full && prev >= 0 && row == prev + 1;
-                        const bool merges = rp.full && next == row + 1;
+                        const bool pairs = rp.full || rp.tmap;
+                        const bool merged_away = pairs && prev >= 0 && row == prev + 1;
+                        const bool merges = pairs && next == row + 1;
                         if (!merged_away) {
                             bytes = merges ? 2 * RB : RB;
                             src = inb + static_cast<int64_t>(row) * pitch;
+                            zrow = row;
                             dst += (l * G + w) * RB;
                         }
                     }
@@ -330,7 +406,13 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
                 const unsigned total = __reduce_add_sync(0xffffffffu, bytes);
                 if (lane == 0) mbar_arrive_expect_tx(&full_z[zslot], total);
                 __syncwarp();
-                if (bytes) tma_load_1d_hint(dst, src, bytes, &full_z[zslot], pol_keep);
+                if (bytes) {
+                    if (rp.tmap)
+                        tma_load_2d_hint(dst, bytes == RB ? &tm.m1 : &tm.m2, p.u_off * 2, zrow,
+                                         &full_z[zslot], pol_keep);
+                    else
+                        tma_load_1d_hint(dst, src, bytes, &full_z[zslot], pol_keep);
+                }
                 if (++zslot == nz) {
                     zslot = 0;
                     zpar ^= 1;
@@ -516,16 +598,14 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     if (!svals) return false;
     // 64-unit slabs (one CTA per SM) unless CHEBFD_OPT_SLAB_UNITS asks for 32 (two CTAs per SM)
     const int us = (units % 64 == 0 && ctx.slab_units != 32) ? 64 : 32;
-    // default (CHEBFD_OPT_RING = 1): where the row-group kernel would run, i.e. the
-    // band-ordered launches (planes beyond the L2 budget); 2: wherever it applies
-    if (ctx.ring == 1) {
-        if (ctx.grouped == 0 || ctx.tiles_per_cta <= 0) return false;
-        StepParams probe{};
-        probe.row0 = s.row0;
-        probe.row1 = s.row1;
-        set_band_order(ctx, a, probe, kTileRows, static_cast<size_t>(std::min(units, 128)) * 16);
-        if (probe.band_tps == 0) return false;
-    }
+    // default (CHEBFD_OPT_RING = 1): lattices whose z-plane of the gathered block exceeds
+    // twice the band budget (32 MB) -- measured with tools/ring_exp.py: C4 (1 GB planes) filter
+    // 7.56 -> 6.36 ms per step, TI 512^2x8 n_b = 32 3.9 -> 3.45, TI 128^2x64 n_b = 64 (64 MB)
+    // 4.5 -> 3.65, n_b = 256 (256 MB, four slabs) 15.5 -> 15.4; TI 64^3 n_b = 64 (16 MB planes,
+    // L2-resident) 1.04 -> 1.15, where the SELL kernel stays.  2: wherever it applies
+    if (ctx.ring == 1 &&
+        static_cast<size_t>(P) * units * 16 <= 2 * static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 0)))
+        return false;
     const size_t rb = static_cast<size_t>(us) * 16;
     const size_t os = (SY + 2) * kGroupRows * rb, zs = SY * kGroupRows * rb + SY * kRingMaxVals * 16;
     const int segx = static_cast<int>(std::min<int64_t>(lx, ctx.ring_segx > 0 ? ctx.ring_segx : 64));
@@ -543,6 +623,13 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         if (strips % d == 0 && static_cast<size_t>(d * SY * Ln) * units * 16 <=
                                    static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 1)))
             spb = d;
+    if (ctx.ring_order != 0) {
+        // a (segment, band) unit of CTAs about fills the GPU: all planes x spb strips
+        spb = 1;
+        for (int64_t d = 1; d <= strips; ++d)
+            if (strips % d == 0 && d * planes <= std::max<int64_t>(ctx.ring_spb_ctas > 0 ? ctx.ring_spb_ctas : ctx.num_sms, planes))
+                spb = d;
+    }
     const int64_t nseg = (lx + segx - 1) / segx;
     const int64_t grid = strips * planes * nseg;
     if (grid >= (int64_t(1) << 31)) return false;
@@ -554,7 +641,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     const bool cv = gm.ring_const_ok && ctx.ring_consts != 0;
     if (!cv) rs = 2;
     if (us == 32 && rs == 4) rs = 2;
-    void (*kernel)(const StepParams, const RingParams, const RingConsts) =
+    void (*kernel)(const StepParams, const RingParams, const RingConsts, const RingMaps) =
         !cv ? (us == 64 ? step_ring_kernel<KIND, 64, 2, false> : step_ring_kernel<KIND, 32, 2, false>)
         : us == 64 ? (rs == 4 ? step_ring_kernel<KIND, 64, 4, true> : step_ring_kernel<KIND, 64, 2, true>)
                    : (rs == 2 ? step_ring_kernel<KIND, 32, 2, true> : step_ring_kernel<KIND, 32, 1, true>);
@@ -613,9 +700,18 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         rp.segx = segx;
         rp.nseg = static_cast<int>(nseg);
         rp.spb = static_cast<int>(spb);
+        rp.nbands = static_cast<int>(strips / spb);
+        rp.order = ctx.ring_order != 0 ? 1 : 0;
         rp.no = no;
         rp.nz = nz;
         rp.full = (us == units && pitch == units) ? 1 : 0;
+        // tensor-map copies: CHEBFD_OPT_RING_TMAP 1 (default) wherever a slab is narrower
+        // than the row, 2 always, 0 never (per-row 1D copies for slabs)
+        RingMaps maps{};
+        rp.tmap = 0;
+        if ((ctx.ring_tmap == 2 || (ctx.ring_tmap == 1 && !rp.full)) &&
+            make_ring_maps(maps, s.in, a.part.ext_rows(), pitch, us))
+            rp.tmap = 1;
         const bool pdl = s.pdl_ok && ctx.pdl == 2;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(grid));
@@ -627,7 +723,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        CFD_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, rp, cc));
+        CFD_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, rp, cc, maps));
         CFD_CUDA(cudaGetLastError());
         ctx.launches++;
         ctx.ring_launches++;

@@ -28,9 +28,11 @@ def bits_equal(a, b):
 def rctx(ctx):
     ctx.set_option("ring", 2)
     yield ctx
-    for k in ("ring", "ring_segx", "ring_no", "ring_nz", "ring_rows"):
+    for k in ("ring_segx", "ring_no", "ring_nz", "ring_rows", "ring_order", "ring_unit"):
         ctx.set_option(k, 0)
+    ctx.set_option("ring", 1)
     ctx.set_option("ring_consts", 1)
+    ctx.set_option("ring_tmap", 1)
     ctx.set_option("delayed_x", 3)
 
 
@@ -53,7 +55,11 @@ def block(A, host):
     ((8, 8, 3), 96, "periodic_xy_open_z"),    # three 32-unit slabs (row copies, not site copies)
     ((8, 4, 3), 128, "periodic_xy_open_z"),   # two 64-unit slabs
 ])
-def test_ring_filter_bitexact(rctx, orc, l, nb, boundary):
+@pytest.mark.parametrize("tmap", [1, 2, 0])
+def test_ring_filter_bitexact(rctx, orc, l, nb, boundary, tmap):
+    """tmap: tensor-map TMA box copies (UTMALDG) for column slabs only (default), always, or
+    never (1D bulk copies, UBLKCP: per row where a slab is narrower than the row)."""
+    rctx.set_option("ring_tmap", tmap)
     A, c = ti(rctx, orc, l, boundary)
     x0 = orc.randomize(c.dim, nb, 5, True)
     p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 17, "lanczos2")
@@ -76,6 +82,25 @@ def test_ring_segments_and_depths(rctx, orc, segx, no, nz):
     A, c = ti(rctx, orc, l)
     x0 = orc.randomize(c.dim, nb, 6, True)
     p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 11, "jackson")
+    xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
+    X = block(A, x0)
+    before = rctx.ring_launches
+    cf.apply_filter(A, X, p)
+    assert rctx.ring_launches > before
+    assert bits_equal(X.to_numpy(), xr)
+
+
+@pytest.mark.parametrize("unit", [0, 4, 9])
+def test_ring_cta_order_x_segments_slowest(rctx, orc, unit):
+    """CTA order 1: (x segment, band of strips, plane, strip) with bands of `unit` / planes
+    strips -- only which CTA computes which rows changes."""
+    l, nb = (8, 16, 3), 64
+    rctx.set_option("ring_order", 1)
+    rctx.set_option("ring_unit", unit)
+    rctx.set_option("ring_segx", 3)
+    A, c = ti(rctx, orc, l)
+    x0 = orc.randomize(c.dim, nb, 9, True)
+    p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 10, "lanczos2")
     xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
     X = block(A, x0)
     before = rctx.ring_launches

@@ -64,7 +64,9 @@ def test_c4_sublattice_apply_filter_bitexact_vs_reference(ctx, ref_mt):
     x0 = cf.host_randomize(m.dim, 64, 3, True)  # = BlockVector::randomize(3), parallel
     X = cf.BlockVector(A, 64).upload(x0)
     p = cf.make_filter((-0.3, 0.3), (-5.6, 5.6), 12, "jackson")
+    ring0 = ctx.ring_launches
     cf.apply_filter(A, X, p)
+    assert ctx.ring_launches - ring0 == 10  # the fused loop ran on the site-ring kernel (default)
     got = X.to_numpy()
     del X
     xr, _ = ref_mt.apply_filter(m, x0, p.combined, p.alpha, p.beta)
