@@ -245,6 +245,16 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
         idx /= static_cast<unsigned>(rp.spb);
         z = static_cast<int>(idx % static_cast<unsigned>(rp.planes));
         band = static_cast<int>(idx / static_cast<unsigned>(rp.planes));
+    } else if (rp.order == 2) {
+        // planes fastest, then strips, x segment slowest: a CTA's z neighbours are its
+        // neighbours in launch order and its y neighbours `planes` CTAs away, so a wave of
+        // CTAs is a compact (strips x planes) brick marching along x in lockstep and a wave
+        // boundary separates one plane pair and `planes` strip pairs at most
+        z = static_cast<int>(idx % static_cast<unsigned>(rp.planes));
+        idx /= static_cast<unsigned>(rp.planes);
+        sb = static_cast<int>(idx % static_cast<unsigned>(rp.spb));
+        q = static_cast<int>(idx / static_cast<unsigned>(rp.spb));
+        band = 0;
     } else {
         // x segment slowest: a wave of CTAs is (all planes) x (spb adjacent strips) of one x
         // segment marching in lockstep, so the strips' y -+ 1 halo lines and z -+ 1 rows are
@@ -623,7 +633,9 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         if (strips % d == 0 && static_cast<size_t>(d * SY * Ln) * units * 16 <=
                                    static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 1)))
             spb = d;
-    if (ctx.ring_order != 0) {
+    if (ctx.ring_order == 2) {
+        spb = strips;
+    } else if (ctx.ring_order != 0) {
         // a (segment, band) unit of CTAs about fills the GPU: all planes x spb strips
         spb = 1;
         for (int64_t d = 1; d <= strips; ++d)
@@ -701,7 +713,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         rp.nseg = static_cast<int>(nseg);
         rp.spb = static_cast<int>(spb);
         rp.nbands = static_cast<int>(strips / spb);
-        rp.order = ctx.ring_order != 0 ? 1 : 0;
+        rp.order = ctx.ring_order;
         rp.no = no;
         rp.nz = nz;
         rp.full = (us == units && pitch == units) ? 1 : 0;

@@ -90,12 +90,12 @@ def test_ring_segments_and_depths(rctx, orc, segx, no, nz):
     assert bits_equal(X.to_numpy(), xr)
 
 
-@pytest.mark.parametrize("unit", [0, 4, 9])
-def test_ring_cta_order_x_segments_slowest(rctx, orc, unit):
+@pytest.mark.parametrize("order,unit", [(1, 0), (1, 4), (1, 9), (2, 0)])
+def test_ring_cta_order_x_segments_slowest(rctx, orc, order, unit):
     """CTA order 1: (x segment, band of strips, plane, strip) with bands of `unit` / planes
-    strips -- only which CTA computes which rows changes."""
+    strips; order 2: (x segment, strip, plane) -- only which CTA computes which rows changes."""
     l, nb = (8, 16, 3), 64
-    rctx.set_option("ring_order", 1)
+    rctx.set_option("ring_order", order)
     rctx.set_option("ring_unit", unit)
     rctx.set_option("ring_segx", 3)
     A, c = ti(rctx, orc, l)
