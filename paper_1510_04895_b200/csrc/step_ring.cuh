@@ -37,6 +37,9 @@
 namespace cfd {
 namespace {
 
+#ifndef CFD_RING_PREFETCH
+#define CFD_RING_PREFETCH 2  // columns ahead the consumers' W / X rows are prefetched into the L2
+#endif
 constexpr int kRingSY = 4;         // lattice lines per strip
 constexpr int kRingMaxDepth = 8;   // ring slots (each ring)
 
@@ -467,15 +470,33 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
                     if constexpr (kind_reads_x(KIND)) xv[r] = lds_pol(&X[own], pol_stream);
                 }
             };
-            T wi[RS], xi[RS];
-            load_rows(xa, wi, xi);
+            // own-row streams (W, X): loaded at the top of the column's step and consumed in
+            // its epilogue -- a whole step later -- after an L2 prefetch kPre columns ahead.
+            // (Handing a next-column register buffer over at the end of a step stalled on
+            // the loads in flight: 23 % of the ncu samples.)
+            constexpr int kPre = CFD_RING_PREFETCH;
+            auto prefetch_rows = [&](int c) {
+#pragma unroll
+                for (int r = 0; r < RS; ++r) {
+                    const int64_t own = (rg0 + static_cast<int64_t>(G) * c + r) * pitch;
+                    if constexpr (kind_reads_w(KIND))
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(&W[own]));
+                    if constexpr (kind_reads_x(KIND))
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(&X[own]));
+                }
+            };
+            if constexpr (kPre > 0) {
+#pragma unroll
+                for (int i = 1; i < kPre; ++i)
+                    if (xa + i < xb) prefetch_rows(xa + i);
+            }
             for (int c = xa; c < xb; ++c) {
                 const int kz = c - xa;
-                // next column's own-row streams: a step of latency hiding in registers
-                T wn[RS], xn[RS];
-#pragma unroll
-                for (int r = 0; r < RS; ++r) wn[r] = xn[r] = T{};
-                if (c + 1 < xb) load_rows(c + 1, wn, xn);
+                T wi[RS], xi[RS];
+                load_rows(c, wi, xi);
+                if constexpr (kPre > 0) {
+                    if (c + kPre < xb) prefetch_rows(c + kPre);
+                }
                 const int need = min(c + 1, jhi - 1) - jlo;
                 while (kw <= need) {
                     mbar_wait(&full_o[wslot], wpar);
@@ -555,11 +576,6 @@ __global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 
                 if (++zslot == nz) {
                     zslot = 0;
                     zpar ^= 1;
-                }
-#pragma unroll
-                for (int r = 0; r < RS; ++r) {
-                    wi[r] = wn[r];
-                    xi[r] = xn[r];
                 }
             }
         };
