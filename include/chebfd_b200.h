@@ -126,7 +126,10 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
  * -- the products take them as kernel-parameter constants and only the four diagonal values
  * per site are read; the builder compares the stored values bit for bit), _TMAP (tensor-map
  * TMA: a site's four rows / a z -+ 1 row pair of a column slab as one 2D box copy; 1 =
- * for slabs narrower than the row (default), 2 = always, 0 = per-row 1D bulk copies). */
+ * for slabs narrower than the row (default), 2 = always, 0 = per-row 1D bulk copies), _ORDER
+ * (CTA order: 0 bands of strips with x segments fastest, 1 x segments slowest, 2 planes fastest
+ * then strips then x segments, 3 = automatic (default): 2 on shallow slabs, else 0; _UNIT: CTAs
+ * per band of order 1). */
 /* CHEBFD_OPT_GROUPED (default 1): dot-free steps that run in the band tile order (lattice
  * operators whose z-planes exceed the L2 budget, CHEBFD_OPT_BAND_BYTES) use the row-group
  * kernel: four consecutive rows -- a lattice site's orbitals -- share one merged list of

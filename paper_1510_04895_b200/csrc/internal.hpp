@@ -294,8 +294,9 @@ struct Context {
     // the block exceeds 2 x band_bytes, 2 wherever it applies; CHEBFD_OPT_RING.  ring_segx / ring_no /
     // ring_nz: x-columns per CTA and ring depths (0: defaults); CHEBFD_OPT_RING_SEGX / _NO / _NZ
     int ring = 1, ring_segx = 0, ring_no = 0, ring_nz = 0;
-    int ring_order = 2;   // CTA order: 0 x segments fastest (bands of band_bytes), 1 x segments slowest in bands of strips,
-                          // 2 (default) planes fastest, then strips, x segments slowest; CHEBFD_OPT_RING_ORDER
+    int ring_order = 3;   // CTA order: 0 x segments fastest (bands of band_bytes), 1 x segments slowest in bands of strips,
+                          // 2 planes fastest, then strips, x segments slowest, 3 (default) 2 on shallow slabs else 0;
+                          // CHEBFD_OPT_RING_ORDER
     int ring_spb_ctas = 0;  // order 1: CTAs per (segment, band) unit (0: the SM count); CHEBFD_OPT_RING_UNIT
     int ring_tmap = 1;    // tensor-map TMA copies: 1 for column slabs, 2 always, 0 never; CHEBFD_OPT_RING_TMAP
     int ring_consts = 1;  // 1: constant off-diagonal values as kernel parameters where the matrix has them; CHEBFD_OPT_RING_CONSTS

@@ -649,9 +649,13 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         if (strips % d == 0 && static_cast<size_t>(d * SY * Ln) * units * 16 <=
                                    static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 1)))
             spb = d;
-    if (ctx.ring_order == 2) {
+    // CTA order 3 (default) = automatic: planes fastest where a wave of CTAs then still spans
+    // eight or more strips (shallow slabs, C4: fused step 7.7 -> 7.4 ms), else bands of strips
+    // with x segments fastest (the C3 lattice's 64 planes: 14.2 against 14.7 ms at n_b = 256)
+    const int order = ctx.ring_order == 3 ? (planes * 8 <= ctx.num_sms ? 2 : 0) : ctx.ring_order;
+    if (order == 2) {
         spb = strips;
-    } else if (ctx.ring_order != 0) {
+    } else if (order != 0) {
         // a (segment, band) unit of CTAs about fills the GPU: all planes x spb strips
         spb = 1;
         for (int64_t d = 1; d <= strips; ++d)
@@ -729,7 +733,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         rp.nseg = static_cast<int>(nseg);
         rp.spb = static_cast<int>(spb);
         rp.nbands = static_cast<int>(strips / spb);
-        rp.order = ctx.ring_order;
+        rp.order = order;
         rp.no = no;
         rp.nz = nz;
         rp.full = (us == units && pitch == units) ? 1 : 0;

@@ -30,7 +30,7 @@ def rctx(ctx):
     yield ctx
     for k in ("ring_segx", "ring_no", "ring_nz", "ring_rows", "ring_unit"):
         ctx.set_option(k, 0)
-    ctx.set_option("ring_order", 2)
+    ctx.set_option("ring_order", 3)
     ctx.set_option("ring", 1)
     ctx.set_option("ring_consts", 1)
     ctx.set_option("ring_tmap", 1)
@@ -91,7 +91,7 @@ def test_ring_segments_and_depths(rctx, orc, segx, no, nz):
     assert bits_equal(X.to_numpy(), xr)
 
 
-@pytest.mark.parametrize("order,unit", [(1, 0), (1, 4), (1, 9), (0, 0)])
+@pytest.mark.parametrize("order,unit", [(1, 0), (1, 4), (1, 9), (0, 0), (2, 0)])
 def test_ring_cta_order_x_segments_slowest(rctx, orc, order, unit):
     """CTA order 1: (x segment, band of strips, plane, strip) with bands of `unit` / planes
     strips; order 2: (x segment, strip, plane) -- only which CTA computes which rows changes."""

@@ -44,7 +44,7 @@ def main():
         for s in args.sets.split(";"):
             opts = dict(kv.split("=") for kv in s.split(",") if kv)
             defaults = {"ring": 1, "ring_segx": 0, "ring_no": 0, "ring_nz": 0, "ring_rows": 0,
-                        "ring_consts": 1, "ring_tmap": 1, "ring_order": 2, "ring_unit": 0, "slab_units": 0, "band_bytes": 16 << 20}
+                        "ring_consts": 1, "ring_tmap": 1, "ring_order": 3, "ring_unit": 0, "slab_units": 0, "band_bytes": 16 << 20}
             for k, d in defaults.items():
                 ctx.set_option(k, int(opts.get(k, d)))
             for k, v in opts.items():
