@@ -209,14 +209,13 @@ __device__ __forceinline__ void ring_mac(const RingBases& b, const double2* vs, 
 // operands in shared memory, which multiplies the resident consumer warps -- the FP64
 // chains of 8 warps per SM do not fill the issue slots (ncu: issue 35 % busy, stalls on
 // fixed-latency dependencies)
-template <int KIND, int US, int RS, bool CV>
-__global__ void __launch_bounds__((kGroupRows / RS) * kRingSY * US + 64, (US == 32 && RS >= 2) ? 2 : 1)
+template <int KIND, int US, int RS, bool CV, int SY = kRingSY>
+__global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 && RS >= 2) ? 2 : 1)
     step_ring_kernel(const StepParams p, const RingParams rp, const __grid_constant__ RingConsts cc,
                      const __grid_constant__ RingMaps tm) {
     using T = double2;
     using O = Ops<true, double2>;
     using M = double2;
-    constexpr int SY = kRingSY;
     constexpr int G = kGroupRows;
     constexpr int NG = G / RS;                      // consumer groups
     constexpr int RB = US * 16;                     // bytes of a row (slab)
@@ -612,18 +611,24 @@ template <int KIND>
 bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
     const Matrix& a = *s.a;
     const GroupedMatrix& gm = a.grp;
-    constexpr int SY = kRingSY;
     if (ctx.ring == 0 || ctx.kernel_variant != 1 || !gm.ok || !gm.ring_ok) return false;
     if (s.dots_mode != 0 || units % 32 != 0) return false;
     const int64_t P = a.plane_rows, Ln = a.line_rows;
     const int64_t nrows = s.row1 - s.row0;
     if (P <= 0 || Ln <= 0 || nrows <= 0 || s.row0 % P != 0 || nrows % P != 0) return false;
     const int64_t lx = Ln / kGroupRows, ly = P / Ln, planes = nrows / P;
-    if (ly % SY != 0 || lx < 1 || lx > (1 << 24) || ly > (1 << 24)) return false;
+    if (ly % kRingSY != 0 || lx < 1 || lx > (1 << 24) || ly > (1 << 24)) return false;
     const void* svals = ring_scaled_values(a, s.alpha);
     if (!svals) return false;
-    // 64-unit slabs (one CTA per SM) unless CHEBFD_OPT_SLAB_UNITS asks for 32 (two CTAs per SM)
-    const int us = (units % 64 == 0 && ctx.slab_units != 32) ? 64 : 32;
+    // 64-unit slabs (one CTA per SM) unless CHEBFD_OPT_SLAB_UNITS asks for 32 (two CTAs per SM).
+    // Blocks of a multiple of 128 columns: 128-unit slabs on strips of two lines -- 2 KB instead
+    // of 1 KB pieces of every row (ncu at n_b = 256: DRAM 63 % of its peak with 1 KB pieces
+    // against 74 % with whole 1 KB rows at n_b = 64) and half the passes over the matrix:
+    // C3 lattice n_b = 256 14.5 -> 13.5 ms per filter step, TI 512^2x4 n_b = 128 6.44 -> 6.15.
+    // CHEBFD_OPT_SLAB_UNITS = 128 / 64 forces either.
+    int us = (units % 64 == 0 && ctx.slab_units != 32) ? 64 : 32;
+    if (units % 128 == 0 && (ctx.slab_units == 128 || (ctx.slab_units == 0 && units >= 128))) us = 128;
+    const int SY = us == 128 ? 2 : kRingSY;
     // default (CHEBFD_OPT_RING = 1): lattices whose z-plane of the gathered block exceeds
     // twice the band budget (32 MB) -- measured with tools/ring_exp.py: C4 (1 GB planes) filter
     // 7.56 -> 6.36 ms per step, TI 512^2x8 n_b = 32 3.9 -> 3.45, TI 128^2x64 n_b = 64 (64 MB)
@@ -669,12 +674,14 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     int rs = ctx.ring_rows > 0 ? ctx.ring_rows : 2;
     if (rs != 4 && rs != 2 && rs != 1) rs = 2;
     if (us == 64 && rs == 1) rs = 2;  // 1024 consumer threads + the producer warp do not fit
+    if (us == 128) rs = 2;
     // constant off-diagonal values (kernel parameters) where the matrix has them
     const bool cv = gm.ring_const_ok && ctx.ring_consts != 0;
     if (!cv) rs = 2;
     if (us == 32 && rs == 4) rs = 2;
     void (*kernel)(const StepParams, const RingParams, const RingConsts, const RingMaps) =
-        !cv ? (us == 64 ? step_ring_kernel<KIND, 64, 2, false> : step_ring_kernel<KIND, 32, 2, false>)
+        us == 128 ? (cv ? step_ring_kernel<KIND, 128, 2, true, 2> : step_ring_kernel<KIND, 128, 2, false, 2>)
+        : !cv ? (us == 64 ? step_ring_kernel<KIND, 64, 2, false> : step_ring_kernel<KIND, 32, 2, false>)
         : us == 64 ? (rs == 4 ? step_ring_kernel<KIND, 64, 4, true> : step_ring_kernel<KIND, 64, 2, true>)
                    : (rs == 2 ? step_ring_kernel<KIND, 32, 2, true> : step_ring_kernel<KIND, 32, 1, true>);
     RingConsts cc{};

@@ -34,6 +34,7 @@ def rctx(ctx):
     ctx.set_option("ring", 1)
     ctx.set_option("ring_consts", 1)
     ctx.set_option("ring_tmap", 1)
+    ctx.set_option("slab_units", 0)
     ctx.set_option("delayed_x", 3)
 
 
@@ -54,7 +55,7 @@ def block(A, host):
     ((8, 12, 4), 32, "periodic_all"),
     ((6, 8, 4), 64, "open_all"),
     ((8, 8, 3), 96, "periodic_xy_open_z"),    # three 32-unit slabs (row copies, not site copies)
-    ((8, 4, 3), 128, "periodic_xy_open_z"),   # two 64-unit slabs
+    ((8, 4, 3), 128, "periodic_xy_open_z"),   # one 128-unit slab on two-line strips
 ])
 @pytest.mark.parametrize("tmap", [1, 2, 0])
 def test_ring_filter_bitexact(rctx, orc, l, nb, boundary, tmap):
@@ -64,6 +65,28 @@ def test_ring_filter_bitexact(rctx, orc, l, nb, boundary, tmap):
     A, c = ti(rctx, orc, l, boundary)
     x0 = orc.randomize(c.dim, nb, 5, True)
     p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 17, "lanczos2")
+    xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
+    X = block(A, x0)
+    before = rctx.ring_launches
+    cf.apply_filter(A, X, p)
+    assert rctx.ring_launches > before
+    assert bits_equal(X.to_numpy(), xr)
+
+
+@pytest.mark.parametrize("nb,slab,consts,boundary", [
+    (256, 0, 1, "periodic_xy_open_z"),    # two 128-unit slabs on two-line strips (the default from 128 columns)
+    (128, 128, 1, "periodic_xy_open_z"),  # one whole-row 128-unit slab (1D bulk copies)
+    (384, 128, 0, "periodic_all"),        # three 128-unit slabs, values from memory
+    (256, 64, 1, "open_all"),             # four 64-unit slabs on four-line strips
+])
+def test_ring_wide_blocks(rctx, orc, nb, slab, consts, boundary):
+    """Blocks wider than a slab: 128-unit slabs run strips of two lattice lines (tensor-map
+    box copies of 4 / 2 / 1 rows x 2 KB), 64-unit slabs strips of four."""
+    rctx.set_option("slab_units", slab)
+    rctx.set_option("ring_consts", consts)
+    A, c = ti(rctx, orc, (8, 8, 3), boundary)
+    x0 = orc.randomize(c.dim, nb, 4, True)
+    p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), 9, "lanczos2")
     xr, _ = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta)
     X = block(A, x0)
     before = rctx.ring_launches

@@ -19,7 +19,8 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 CASES = {"c4": ((512, 512, 8), 64), "c3_256": ((128, 128, 64), 256), "c3_64": ((128, 128, 64), 64),
          "c3_32": ((128, 128, 64), 32), "c2": ((64, 64, 64), 32), "c2_64": ((64, 64, 64), 64),
-         "c4_32": ((512, 512, 8), 32), "c4_128": ((512, 512, 4), 128)}
+         "c4_32": ((512, 512, 8), 32), "c4_128": ((512, 512, 4), 128),
+         "c4_256": ((512, 512, 2), 256)}
 
 
 def main():
