@@ -491,8 +491,12 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
             }
             for (int c = xa; c < xb; ++c) {
                 const int kz = c - xa;
+                const int4 pb = plan_s[(l * segx + kz) * 2 + 1];
+                const int pat = pb.z;
+                // static sites load their own rows now (consumed a whole step later); generic
+                // sites after their gathers, whose registers they would otherwise take
                 T wi[RS], xi[RS];
-                load_rows(c, wi, xi);
+                if (pat != 0) load_rows(c, wi, xi);
                 if constexpr (kPre > 0) {
                     if (c + kPre < xb) prefetch_rows(c + kPre);
                 }
@@ -506,7 +510,6 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
                     }
                 }
                 mbar_wait(&full_z[zslot], zpar);
-                const int4 pb = plan_s[(l * segx + kz) * 2 + 1];
                 const unsigned char* oc = oring + static_cast<size_t>(so_c) * OS + u * 16;
                 const unsigned char* om = oring + static_cast<size_t>(so_m) * OS + u * 16;
                 const unsigned char* op = oring + static_cast<size_t>(so_p) * OS + u * 16;
@@ -523,7 +526,6 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
                 T acc[RS], ui[RS];
 #pragma unroll
                 for (int r = 0; r < RS; ++r) acc[r] = O::zero();
-                const int pat = pb.z;
                 if (pat == 1) {
                     ring_mac<PatTiMid, RB, R0, RS, CV>(b, vs, cc, acc, ui);
                 } else if (pat == 2) {
@@ -540,23 +542,39 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
                     const int n = pa.z;
                     constexpr unsigned SUB = ((1u << RS) - 1u) << R0;
                     int vi = 0;
-#pragma unroll 4
-                    for (int k = 0; k < n; ++k) {
-                        const unsigned cw = static_cast<unsigned>(__ldg(cl + k));
-                        const unsigned m = cw >> 28;
-                        if (m & SUB) {
-                            const T g = ldg(&inu[static_cast<int64_t>(cw & 0x0FFFFFFFu) * pitch]);
+                    // batches of eight columns: their gathers are all in flight before the
+                    // first product (whole lines of such sites sit on the y wrap: two strips
+                    // per plane run at this path's speed)
+                    const int4* cl4 = reinterpret_cast<const int4*>(cl);
+                    for (int k0 = 0; k0 < n; k0 += 8) {
+                        const int4 ca = __ldg(cl4 + (k0 >> 2));
+                        const int4 cb = k0 + 4 < n ? __ldg(cl4 + (k0 >> 2) + 1) : make_int4(0, 0, 0, 0);
+                        const unsigned cw[8] = {static_cast<unsigned>(ca.x), static_cast<unsigned>(ca.y),
+                                                static_cast<unsigned>(ca.z), static_cast<unsigned>(ca.w),
+                                                static_cast<unsigned>(cb.x), static_cast<unsigned>(cb.y),
+                                                static_cast<unsigned>(cb.z), static_cast<unsigned>(cb.w)};
+                        T g[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            g[j] = T{};
+                            if ((cw[j] >> 28) & SUB)
+                                g[j] = ldg(&inu[static_cast<int64_t>(cw[j] & 0x0FFFFFFFu) * pitch]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const unsigned m = cw[j] >> 28;
 #pragma unroll
                             for (int r = 0; r < RS; ++r)
                                 if (m & (1u << (R0 + r)))
                                     acc[r] = O::vadd(
-                                        acc[r], O::prod(vs[vi + __popc(m & ((1u << (R0 + r)) - 1u))], g));
+                                        acc[r], O::prod(vs[vi + __popc(m & ((1u << (R0 + r)) - 1u))], g[j]));
+                            vi += __popc(m);
                         }
-                        vi += __popc(m);
                     }
 #pragma unroll
                     for (int r = 0; r < RS; ++r)
                         ui[r] = *reinterpret_cast<const T*>(b.own + (R0 + r) * RB);
+                    load_rows(c, wi, xi);
                 }
 #pragma unroll
                 for (int r = 0; r < RS; ++r)
