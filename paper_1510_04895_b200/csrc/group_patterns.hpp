@@ -30,6 +30,20 @@ struct PatBase {
         for (int q = 0; q < r; ++q) n += (D::m(k) >> q) & 1;
         return n;
     }
+    // x / y neighbour columns (positions 0..7 and 12..19 after the z-1 columns) are read by
+    // the two rows of one row pair (mask 0x3 or 0xC), with values of equal magnitude: every
+    // nonzero entry of hop[j] = -t (G1 - i G^{j+1}) / 2 is +-t/2 or +-i t/2 (models.cpp:88-93).
+    // pair_neg(k): the upper row's real / imaginary part has the opposite sign to the lower
+    // row's, so both rows' products are +-(v g_r), +-(v g_i) of ONE value v: two multiplies per
+    // column instead of four ((-v) g = -(v g) and a + (-p) = a - p exactly).  The launcher
+    // checks the relation on the actual values (step_ring.cuh run_ring).
+    __host__ __device__ static constexpr bool pair_col(int k) {
+        const int q = k - (D::OWN - 8);
+        return ((q >= 0 && q < 8) || (q >= 12 && q < 20)) && (D::m(k) == 0x3u || D::m(k) == 0xCu);
+    }
+    __host__ __device__ static constexpr bool pair_neg(int k) {
+        return (0x930C6u >> (k - (D::OWN - 8))) & 1u;
+    }
 };
 struct PatTiMid : PatBase<PatTiMid> {
     static constexpr int NC = 24, OWN = 10, ID = 0;

@@ -40,6 +40,9 @@ namespace {
 #ifndef CFD_RING_PREFETCH
 #define CFD_RING_PREFETCH 2  // columns ahead the consumers' W / X rows are prefetched into the L2
 #endif
+#ifndef CFD_RING_SHARE
+#define CFD_RING_SHARE 1  // row pairs share the products of an x / y neighbour column (PatBase::pair_col)
+#endif
 constexpr int kRingSY = 4;         // lattice lines per strip
 constexpr int kRingMaxDepth = 8;   // ring slots (each ring)
 
@@ -172,7 +175,30 @@ __device__ __forceinline__ void ring_mac(const RingBases& b, const double2* vs, 
     ring_for<P::NC>([&](auto kt) {
         constexpr int k = decltype(kt)::value;
         constexpr bool own = k >= P::OWN + R0 && k < P::OWN + R0 + RS;
-        if constexpr ((P::m(k) & SUB) != 0u || own) {
+        constexpr bool shared_pair = CFD_RING_SHARE != 0 && CV && RS == 2 && P::pair_col(k) && (P::m(k) & SUB) == SUB;
+        if constexpr (shared_pair) {
+            // both rows of this thread's pair read column k with values +-v / +-iv of one
+            // magnitude: the two products v g_r, v g_i serve both rows
+            static_assert((((P::re(k) | P::im(k)) & SUB) == SUB) && !own, "pair column: purely real / imaginary values");
+            const double2 gk = ring_operand<P, k, RB>(b);
+            const double v = cc.v[P::ID][P::voff(k, R0)];
+            const double px = mul(v, gk.x), py = mul(v, gk.y);
+            if constexpr ((P::re(k) >> R0) & 1u) {
+                acc[0].x = add(acc[0].x, px);
+                acc[0].y = add(acc[0].y, py);
+            } else {
+                acc[0].x = sub(acc[0].x, py);
+                acc[0].y = add(acc[0].y, px);
+            }
+            constexpr bool neg = P::pair_neg(k);
+            if constexpr ((P::re(k) >> (R0 + 1)) & 1u) {
+                acc[1].x = neg ? sub(acc[1].x, px) : add(acc[1].x, px);
+                acc[1].y = neg ? sub(acc[1].y, py) : add(acc[1].y, py);
+            } else {
+                acc[1].x = neg ? add(acc[1].x, py) : sub(acc[1].x, py);
+                acc[1].y = neg ? sub(acc[1].y, px) : add(acc[1].y, px);
+            }
+        } else if constexpr ((P::m(k) & SUB) != 0u || own) {
             const double2 gk = ring_operand<P, k, RB>(b);
             ring_for<RS>([&](auto rt) {
                 constexpr int r = R0 + decltype(rt)::value;
@@ -694,14 +720,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     if (us == 64 && rs == 1) rs = 2;  // 1024 consumer threads + the producer warp do not fit
     if (us == 128) rs = 2;
     // constant off-diagonal values (kernel parameters) where the matrix has them
-    const bool cv = gm.ring_const_ok && ctx.ring_consts != 0;
-    if (!cv) rs = 2;
-    if (us == 32 && rs == 4) rs = 2;
-    void (*kernel)(const StepParams, const RingParams, const RingConsts, const RingMaps) =
-        us == 128 ? (cv ? step_ring_kernel<KIND, 128, 2, true, 2> : step_ring_kernel<KIND, 128, 2, false, 2>)
-        : !cv ? (us == 64 ? step_ring_kernel<KIND, 64, 2, false> : step_ring_kernel<KIND, 32, 2, false>)
-        : us == 64 ? (rs == 4 ? step_ring_kernel<KIND, 64, 4, true> : step_ring_kernel<KIND, 64, 2, true>)
-                   : (rs == 2 ? step_ring_kernel<KIND, 32, 2, true> : step_ring_kernel<KIND, 32, 1, true>);
+    bool cv = gm.ring_const_ok && ctx.ring_consts != 0;
     RingConsts cc{};
     if (cv) {
         // the value a product uses: the real or the imaginary part, scaled as the grouped
@@ -720,7 +739,30 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         fill(PatTiMid{});
         fill(PatTiLo{});
         fill(PatTiHi{});
+        // the row pairs' shared products (PatBase::pair_col) hold for these values?  Else the
+        // kernels that read every value from memory
+        bool share_ok = true;
+        auto check = [&](auto pat) {
+            using P = decltype(pat);
+            for (int k = 0; k < P::NC; ++k) {
+                if (!P::pair_col(k)) continue;
+                const int ra = P::m(k) == 0x3u ? 0 : 2;
+                const double va = cc.v[P::ID][P::voff(k, ra)], vb = cc.v[P::ID][P::voff(k, ra + 1)];
+                if (va == 0.0 || !(vb == (P::pair_neg(k) ? -va : va))) share_ok = false;
+            }
+        };
+        check(PatTiMid{});
+        check(PatTiLo{});
+        check(PatTiHi{});
+        if (CFD_RING_SHARE != 0 && !share_ok) cv = false;
     }
+    if (!cv) rs = 2;
+    if (us == 32 && rs == 4) rs = 2;
+    void (*kernel)(const StepParams, const RingParams, const RingConsts, const RingMaps) =
+        us == 128 ? (cv ? step_ring_kernel<KIND, 128, 2, true, 2> : step_ring_kernel<KIND, 128, 2, false, 2>)
+        : !cv ? (us == 64 ? step_ring_kernel<KIND, 64, 2, false> : step_ring_kernel<KIND, 32, 2, false>)
+        : us == 64 ? (rs == 4 ? step_ring_kernel<KIND, 64, 4, true> : step_ring_kernel<KIND, 64, 2, true>)
+                   : (rs == 2 ? step_ring_kernel<KIND, 32, 2, true> : step_ring_kernel<KIND, 32, 1, true>);
     static thread_local std::map<std::pair<const void*, int>, size_t> attr_set;
     auto& cur = attr_set[std::make_pair(reinterpret_cast<const void*>(kernel), ctx.device)];
     if (cur < smem) {

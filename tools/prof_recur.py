@@ -18,8 +18,12 @@ def main():
     ap.add_argument("--lattice", type=int, nargs=3, default=[512, 512, 8])
     ap.add_argument("--nb", type=int, default=64)
     ap.add_argument("--launches", type=int, default=3)
+    ap.add_argument("--opt", action="append", default=[], help="context option name=value (repeatable)")
     args = ap.parse_args()
     ctx = cf.Context(0)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     A = cf.SparseMatrix.topological_insulator(ctx, cf.LatticeSpec(*args.lattice, disorder=0.5, seed=1))
     p = cf.make_filter((-0.3, 0.3), (-5.6, 5.6), 4, "lanczos2")
     cf.apply_filter(A, cf.BlockVector(A, 1).randomize_device(1), p)  # builds the scaled values
