@@ -110,7 +110,8 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
        CHEBFD_OPT_GROUPED = 21, CHEBFD_OPT_GROUP_LINES = 22, CHEBFD_OPT_RING = 23,
        CHEBFD_OPT_RING_SEGX = 24, CHEBFD_OPT_RING_NO = 25, CHEBFD_OPT_RING_NZ = 26,
        CHEBFD_OPT_RING_ROWS = 27, CHEBFD_OPT_RING_CONSTS = 28,
-       CHEBFD_OPT_RING_TMAP = 29, CHEBFD_OPT_RING_ORDER = 30, CHEBFD_OPT_RING_UNIT = 31 };
+       CHEBFD_OPT_RING_TMAP = 29, CHEBFD_OPT_RING_ORDER = 30, CHEBFD_OPT_RING_UNIT = 31,
+       CHEBFD_OPT_RING_DOTS = 32 };
 /* CHEBFD_OPT_RING: the site-ring step kernel (csrc/step_ring.cuh) on complex TI lattice
  * operators with blocks of a multiple of 32 columns: a producer warp stages each x-column of
  * a strip of four lattice lines (site blocks, z -+ 1 rows, matrix values) in shared-memory
@@ -129,7 +130,10 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
  * for slabs narrower than the row (default), 2 = always, 0 = per-row 1D bulk copies), _ORDER
  * (CTA order: 0 bands of strips with x segments fastest, 1 x segments slowest, 2 planes fastest
  * then strips then x segments, 3 = automatic (default): 2 on shallow slabs, else 0; _UNIT: CTAs
- * per band of order 1). */
+ * per band of order 1), _DOTS (default 1: the V_n-only steps that carry the doubling moment
+ * sums -- apply_filter with moments, kpm_dos -- also run the site-ring kernel when the step is
+ * one launch; per-CTA partials reduced in CTA index order, bitwise reproducible; 0: those
+ * steps keep the row-group / SELL kernels). */
 /* CHEBFD_OPT_GROUPED (default 1): dot-free steps that run in the band tile order (lattice
  * operators whose z-planes exceed the L2 budget, CHEBFD_OPT_BAND_BYTES) use the row-group
  * kernel: four consecutive rows -- a lattice site's orbitals -- share one merged list of

@@ -195,7 +195,7 @@ class Context:
                 "compact_halo": 19, "gram": 20, "grouped": 21, "group_lines": 22,
                 "ring": 23, "ring_segx": 24, "ring_no": 25, "ring_nz": 26,
                 "ring_rows": 27, "ring_consts": 28, "ring_tmap": 29,
-                "ring_order": 30, "ring_unit": 31}[name]
+                "ring_order": 30, "ring_unit": 31, "ring_dots": 32}[name]
         if name == "moments" and isinstance(value, str):
             value = {"direct": 0, "doubling": 1}[value]
         if name == "kernel" and isinstance(value, str):

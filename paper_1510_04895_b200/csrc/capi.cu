@@ -1083,6 +1083,8 @@ int chebfd_ctx_set_option(chebfd_ctx* ctx, int option, int64_t value) {
             c->ring_order = static_cast<int>(value);
         else if (option == CHEBFD_OPT_RING_UNIT)
             c->ring_spb_ctas = static_cast<int>(value);
+        else if (option == CHEBFD_OPT_RING_DOTS)
+            c->ring_dots = static_cast<int>(value);
         else if (option == CHEBFD_OPT_TILES_PER_CTA)
             c->tiles_per_cta = static_cast<int>(std::max<int64_t>(value, 0));
         else if (option == CHEBFD_OPT_PAIR_TILE_ROWS)

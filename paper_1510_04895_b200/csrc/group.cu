@@ -384,6 +384,7 @@ static void build_ring_plan(Matrix& m, cudaStream_t st) {
     CFD_CUDA(cudaStreamSynchronize(st));
     if (h != 0) return;
     for (int q = 0; q < 3; ++q) {
+        gm.ring_pat_present[q] = hf[q] != ~0ull;
         if (hf[q] == ~0ull) continue;  // pattern absent: its constants are never used
         int4 pb;
         CFD_CUDA(cudaMemcpy(&pb, gm.ring_plan.as<int4>() + 2 * hf[q] + 1, sizeof(int4),

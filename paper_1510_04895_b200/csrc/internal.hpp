@@ -152,6 +152,7 @@ struct GroupedMatrix {
     // four diagonal (disorder) values per site from memory
     bool ring_const_ok = false;
     double ring_consts[3][44][2] = {};
+    bool ring_pat_present[3] = {};  // the lattice holds sites of this pattern (else its constants are unset)
 };
 constexpr int kRingMaxVals = 44;  // values per site staged by the site-ring kernel
 
@@ -300,6 +301,7 @@ struct Context {
     int ring_spb_ctas = 0;  // order 1: CTAs per (segment, band) unit (0: the SM count); CHEBFD_OPT_RING_UNIT
     int ring_tmap = 1;    // tensor-map TMA copies: 1 for column slabs, 2 always, 0 never; CHEBFD_OPT_RING_TMAP
     int ring_consts = 1;  // 1: constant off-diagonal values as kernel parameters where the matrix has them; CHEBFD_OPT_RING_CONSTS
+    int ring_dots = 1;  // 1: V_n-only steps with doubling moment sums (DMODE 4 / 5 / 6) on the site-ring kernel; CHEBFD_OPT_RING_DOTS
     int ring_rows = 0;  // rows of a site per consumer thread (4, 2, 1; 0: default 2); CHEBFD_OPT_RING_ROWS
     int64_t ring_launches = 0;   // step launches that ran the site-ring kernel
     // exchange only the referenced halo rows of structurally symmetric operators (lattice

@@ -177,7 +177,9 @@ constexpr int kReduceGroup = 32;
 // partial rows a grid reduction over n CTA partials needs (its group sums included)
 __host__ __device__ constexpr int64_t reduce_rows_needed(int64_t n) { return n + (n + kReduceGroup - 1) / kReduceGroup; }
 
-template <class T, int NDOT, class Emit>
+// GUARD: the CTA has more than R * US threads (the site-ring kernel's producer warps); the
+// extra threads only take part in the barriers.
+template <class T, int NDOT, bool GUARD = false, class Emit>
 __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1], int R, int US,
                                             T* partials, int part_slot, int nparts, bool final_launch,
                                             unsigned* counter, Emit emit) {
@@ -186,8 +188,11 @@ __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1],
     const int t = threadIdx.x;
     const int rr = t / US, u = t - rr * US;
     const int nthr = R * US;
+    const bool part = !GUARD || t < nthr;
+    if (part) {
 #pragma unroll
-    for (int d = 0; d < NDOT; ++d) sred[d * nthr + t] = acc[d];
+        for (int d = 0; d < NDOT; ++d) sred[d * nthr + t] = acc[d];
+    }
     __syncthreads();
     if (rr == 0) {
 #pragma unroll
@@ -210,6 +215,7 @@ __device__ __forceinline__ void grid_reduce(const T (&acc)[NDOT > 0 ? NDOT : 1],
             auto at = [&](int q) {
                 return ldcg_t(&src[(static_cast<int64_t>(first + q) * NDOT + d) * US + u]);
             };
+            if (!part) continue;
             T s = T{};
             int q = rr;
             if (q < count) {

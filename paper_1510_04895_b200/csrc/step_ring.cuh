@@ -235,7 +235,11 @@ __device__ __forceinline__ void ring_mac(const RingBases& b, const double2* vs, 
 // operands in shared memory, which multiplies the resident consumer warps -- the FP64
 // chains of 8 warps per SM do not fill the issue slots (ncu: issue 35 % busy, stalls on
 // fixed-latency dependencies)
-template <int KIND, int US, int RS, bool CV, int SY = kRingSY>
+//
+// DMODE 4 / 5 / 6 (V_n-only steps of a moment-collecting filter or a KPM run): the raw moment
+// sums of step_epilogue from the consumers' registers; per-thread sums over the CTA's columns
+// in order -> CTA partials -> grid_reduce in CTA index order (bitwise reproducible).
+template <int KIND, int US, int RS, bool CV, int SY = kRingSY, int DMODE = 0>
 __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 && RS >= 2) ? 2 : 1)
     step_ring_kernel(const StepParams p, const RingParams rp, const __grid_constant__ RingConsts cc,
                      const __grid_constant__ RingMaps tm) {
@@ -256,6 +260,9 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
     uint64_t* empty_o = bars + kRingMaxDepth;
     uint64_t* full_z = bars + 2 * kRingMaxDepth;
     uint64_t* empty_z = bars + 3 * kRingMaxDepth;
+    constexpr int NDOT = dots_of(DMODE);
+    static_assert(NDOT == 0 || (KIND == kStepRecur && DMODE >= 4), "ring dots: moment sums of V_n-only steps");
+    double acc_d[NDOT > 0 ? NDOT : 1] = {}, comp_d[NDOT > 0 ? NDOT : 1] = {};
     const int t = threadIdx.x;
     const int no = rp.no, nz = rp.nz;
     unsigned char* oring = smem_raw;
@@ -475,7 +482,6 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
 
         auto consume = [&](auto r0_tag) {
             constexpr int R0 = decltype(r0_tag)::value;
-            double dummy_a[1] = {0.0}, dummy_c[1] = {0.0};
             // ring positions, advanced per column (no divisions in the loop)
             int so_m = no - 1, so_c = 0, so_p = 1 % no;    // slots of columns c - 1, c, c + 1
             if (xa > jlo) {
@@ -604,10 +610,10 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
                 }
 #pragma unroll
                 for (int r = 0; r < RS; ++r)
-                    step_epilogue<O, T, KIND, 0>(acc[r], ui[r], wi[r], xi[r], T{},
-                                                 (rg0 + static_cast<int64_t>(G) * c + r) * pitch, W, X,
-                                                 static_cast<T*>(nullptr), p.beta, coeff, c1, c2,
-                                                 dummy_a, dummy_c);
+                    step_epilogue<O, T, KIND, DMODE>(acc[r], ui[r], wi[r], xi[r], T{},
+                                                     (rg0 + static_cast<int64_t>(G) * c + r) * pitch, W, X,
+                                                     static_cast<T*>(nullptr), p.beta, coeff, c1, c2,
+                                                     acc_d, comp_d);
                 __syncwarp();
                 if (lane0) {
                     mbar_arrive(&empty_z[zslot]);
@@ -640,6 +646,15 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
                 consume(std::integral_constant<int, 3>{});
         }
     }
+    if constexpr (NDOT > 0) {
+        __syncthreads();  // every staged column was consumed: the rings' shared memory is free
+        const int uoff = p.u_off;
+        double* outp = static_cast<double*>(p.dots_out);
+        const int64_t dstride = p.dots_row_stride;
+        grid_reduce<double, NDOT, true>(acc_d, NG * NCT / US, US, static_cast<double*>(p.partials),
+                                        p.part_base + blockIdx.x, p.nparts, p.final_launch != 0, p.counter,
+                                        [&](int d, int uu, double vv) { outp[d * dstride + uoff + uu] = vv; });
+    }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
@@ -651,12 +666,16 @@ inline const void* ring_scaled_values(const Matrix& a, double s) {
 }
 
 // Launch the site-ring kernel for s if it applies; false = nothing launched.
-template <int KIND>
+template <int KIND, int DMODE = 0>
 bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
     const Matrix& a = *s.a;
     const GroupedMatrix& gm = a.grp;
+    constexpr int NDOT = dots_of(DMODE);
     if (ctx.ring == 0 || ctx.kernel_variant != 1 || !gm.ok || !gm.ring_ok) return false;
-    if (s.dots_mode != 0 || units % 32 != 0) return false;
+    if (s.dots_mode != DMODE || units % 32 != 0) return false;
+    // moment sums: whole-step launches only (a rank's interior / boundary launches keep the
+    // kernels whose partial layout they share); CHEBFD_OPT_RING_DOTS = 0: never
+    if (NDOT > 0 && (ctx.ring_dots == 0 || s.partial_base != 0 || !s.final_launch)) return false;
     const int64_t P = a.plane_rows, Ln = a.line_rows;
     const int64_t nrows = s.row1 - s.row0;
     if (P <= 0 || Ln <= 0 || nrows <= 0 || s.row0 % P != 0 || nrows % P != 0) return false;
@@ -714,6 +733,13 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     const int64_t nseg = (lx + segx - 1) / segx;
     const int64_t grid = strips * planes * nseg;
     if (grid >= (int64_t(1) << 31)) return false;
+    if (NDOT > 0) {
+        // the partial rows must fit the context's buffer as it is (graphs hold its address) and
+        // the group tickets its 4 KB of counters
+        if (!gm.ring_const_ok || ctx.ring_consts == 0 || grid > 32 * 1000) return false;
+        if (static_cast<size_t>(reduce_rows_needed(grid)) * NDOT * us * sizeof(double) > ctx.partials.bytes) return false;
+        ctx.counter.ensure(4096);
+    }
     // rows per consumer thread: 2 by default (16 consumer warps per 64-unit strip CTA)
     int rs = ctx.ring_rows > 0 ? ctx.ring_rows : 2;
     if (rs != 4 && rs != 2 && rs != 1) rs = 2;
@@ -744,6 +770,7 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         bool share_ok = true;
         auto check = [&](auto pat) {
             using P = decltype(pat);
+            if (!gm.ring_pat_present[P::ID]) return;  // no site runs this pattern
             for (int k = 0; k < P::NC; ++k) {
                 if (!P::pair_col(k)) continue;
                 const int ra = P::m(k) == 0x3u ? 0 : 2;
@@ -758,11 +785,16 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     }
     if (!cv) rs = 2;
     if (us == 32 && rs == 4) rs = 2;
+    if (NDOT > 0 && (!cv || rs != 2)) return false;
     void (*kernel)(const StepParams, const RingParams, const RingConsts, const RingMaps) =
         us == 128 ? (cv ? step_ring_kernel<KIND, 128, 2, true, 2> : step_ring_kernel<KIND, 128, 2, false, 2>)
         : !cv ? (us == 64 ? step_ring_kernel<KIND, 64, 2, false> : step_ring_kernel<KIND, 32, 2, false>)
         : us == 64 ? (rs == 4 ? step_ring_kernel<KIND, 64, 4, true> : step_ring_kernel<KIND, 64, 2, true>)
                    : (rs == 2 ? step_ring_kernel<KIND, 32, 2, true> : step_ring_kernel<KIND, 32, 1, true>);
+    if constexpr (NDOT > 0)
+        kernel = us == 128  ? step_ring_kernel<KIND, 128, 2, true, 2, DMODE>
+                 : us == 64 ? step_ring_kernel<KIND, 64, 2, true, kRingSY, DMODE>
+                            : step_ring_kernel<KIND, 32, 2, true, kRingSY, DMODE>;
     static thread_local std::map<std::pair<const void*, int>, size_t> attr_set;
     auto& cur = attr_set[std::make_pair(reinterpret_cast<const void*>(kernel), ctx.device)];
     if (cur < smem) {
@@ -789,6 +821,13 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
         p.c2 = s.c2;
         p.coeff_dev = s.coeff_dev;
         p.coeff_index = s.coeff_index;
+        p.dots_out = s.dots_out;
+        p.dots_row_stride = units;
+        p.partials = ctx.partials.p;
+        p.part_base = 0;
+        p.nparts = static_cast<int>(grid);
+        p.final_launch = 1;
+        p.counter = ctx.counter.as<unsigned>();
         RingParams rp{};
         rp.plan = gm.ring_plan.as<int4>();
         rp.cols = gm.cols.as<int>();
@@ -833,7 +872,13 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
 }
 
 inline bool dispatch_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int pitch) {
-    if (s.dots_mode != 0) return false;
+    if (s.dots_mode != 0) {
+        if (s.kind_step != kStepRecur) return false;
+        if (s.dots_mode == 4) return run_ring<kStepRecur, 4>(ctx, s, st, units, pitch);
+        if (s.dots_mode == 5) return run_ring<kStepRecur, 5>(ctx, s, st, units, pitch);
+        if (s.dots_mode == 6) return run_ring<kStepRecur, 6>(ctx, s, st, units, pitch);
+        return false;
+    }
     switch (s.kind_step) {
         case kStepFused: return run_ring<kStepFused>(ctx, s, st, units, pitch);
         case kStepRecur: return run_ring<kStepRecur>(ctx, s, st, units, pitch);

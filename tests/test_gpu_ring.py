@@ -34,6 +34,7 @@ def rctx(ctx):
     ctx.set_option("ring", 1)
     ctx.set_option("ring_consts", 1)
     ctx.set_option("ring_tmap", 1)
+    ctx.set_option("ring_dots", 1)
     ctx.set_option("slab_units", 0)
     ctx.set_option("delayed_x", 3)
 
@@ -154,6 +155,53 @@ def test_ring_rows_per_thread(rctx, orc, rows, l, nb, boundary, consts):
     cf.apply_filter(A, X, p)
     assert rctx.ring_launches > before
     assert bits_equal(X.to_numpy(), xr)
+
+
+@pytest.mark.parametrize("delayed", [3, 2])
+@pytest.mark.parametrize("l,nb,boundary,segx", [
+    ((8, 8, 5), 64, "periodic_xy_open_z", 0),
+    ((8, 12, 4), 32, "periodic_all", 3),        # two CTAs per SM, x segments with aprons
+    ((6, 8, 3), 64, "open_all", 4),             # generic sites on every edge
+    ((8, 4, 3), 256, "periodic_xy_open_z", 0),  # two 128-unit slabs: one reduction per slab
+    ((8, 8, 3), 128, "periodic_xy_open_z", 5),
+])
+def test_ring_moment_steps(rctx, orc, l, nb, boundary, segx, delayed):
+    """V_n-only steps that carry the doubling moment sums (DMODE 5 / 6 of a triple, 4 / 6 of a
+    pair) on the site-ring kernel (CHEBFD_OPT_RING_DOTS): X bit-exact, the MomentTable
+    (filter.hpp:61-68, 86-113) within 1e-12 of the oracle's direct sums, bitwise equal between
+    two runs (per-CTA partials reduced in CTA index order), and more ring launches than with
+    the option off."""
+    rctx.set_option("ring_segx", segx)
+    rctx.set_option("delayed_x", delayed)
+    A, c = ti(rctx, orc, l, boundary)
+    x0 = orc.randomize(c.dim, nb, 21, True)
+    for deg in (12, 31):
+        p = cf.make_filter((-0.3, 0.2), (-5.6, 5.6), deg, "jackson")
+        xr, mr = orc.apply_filter(c, x0, p.combined, p.alpha, p.beta, want_moments=True)
+        runs = []
+        for dots in (0, 1, 1):
+            rctx.set_option("ring_dots", dots)
+            X = block(A, x0)
+            before = rctx.ring_launches
+            mom = cf.apply_filter(A, X, p, want_moments=True)
+            runs.append((rctx.ring_launches - before, mom.m.copy()))
+            assert bits_equal(X.to_numpy(), xr)
+            assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0])), (deg, dots)
+        assert runs[1][0] > runs[0][0], "moment steps did not run the ring kernel"
+        assert bits_equal(runs[1][1], runs[2][1])
+
+
+def test_ring_kpm_dos(rctx, orc):
+    """kpm_dos (spectral.cpp:156-205) with its doubling steps (DMODE 4) on the ring kernel
+    agrees with the row-group / SELL kernels' moments to rounding."""
+    A, c = ti(rctx, orc, (8, 8, 4))
+    mus = []
+    for dots in (0, 1):
+        rctx.set_option("ring_dots", dots)
+        before = rctx.ring_launches
+        mus.append((cf.kpm_dos(A, (-5.6, 5.6), 64, 32, seed=3).moments.copy(), rctx.ring_launches - before))
+    assert mus[1][1] > mus[0][1]
+    assert np.max(np.abs(mus[1][0] - mus[0][0])) <= 1e-12 * abs(mus[0][0][0])
 
 
 @pytest.mark.parametrize("delayed", [0, 2, 3])
