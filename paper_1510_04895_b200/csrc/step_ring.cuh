@@ -697,8 +697,10 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     // 7.56 -> 6.36 ms per step, TI 512^2x8 n_b = 32 3.9 -> 3.45, TI 128^2x64 n_b = 64 (64 MB)
     // 4.5 -> 3.65, n_b = 256 (256 MB, four slabs) 15.5 -> 15.4; TI 64^3 n_b = 64 (16 MB planes,
     // L2-resident) 1.04 -> 1.15, where the SELL kernel stays.  2: wherever it applies
+    // (planes of exactly 32 MB -- the C3 lattice at n_b = 32, the KPM block of its solve -- run
+    // the ring kernel: filter 2.21 -> 1.97 ms per step, KPM of order 2000 2.95 -> 2.55 s)
     if (ctx.ring == 1 &&
-        static_cast<size_t>(P) * units * 16 <= 2 * static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 0)))
+        static_cast<size_t>(P) * units * 16 < 2 * static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 0)))
         return false;
     const size_t rb = static_cast<size_t>(us) * 16;
     const size_t os = (SY + 2) * kGroupRows * rb, zs = SY * kGroupRows * rb + SY * kRingMaxVals * 16;
