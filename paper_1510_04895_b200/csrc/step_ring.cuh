@@ -492,13 +492,21 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
             int wslot = 0, wpar = 0, kw = 0;  // next own-plane column to wait for
             int zslot = 0, zpar = 0;
             const int64_t rg0 = G * (site0 + static_cast<int64_t>(l) * lx) + R0;
-            auto load_rows = [&](int c, T (&wv)[RS], T (&xv)[RS]) {
+            // the own rows of the current column as running pointers (a column ahead = colstep
+            // elements): recomputing (row) * pitch per access cost ~45 of the ~250 instructions
+            // a warp spends on a column
+            const int64_t colstep = static_cast<int64_t>(G) * pitch;
+            T* wrow[RS];
+            // X's rows sit at a launch-uniform distance from W's (no second pointer set)
+            const int64_t xdelta = static_cast<T*>(p.x) - static_cast<T*>(p.w);
+#pragma unroll
+            for (int r = 0; r < RS; ++r) wrow[r] = W + (rg0 + static_cast<int64_t>(G) * xa + r) * pitch;
+            auto load_rows = [&](T (&wv)[RS], T (&xv)[RS]) {
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {
-                    const int64_t own = (rg0 + static_cast<int64_t>(G) * c + r) * pitch;
                     wv[r] = xv[r] = T{};
-                    if constexpr (kind_reads_w(KIND)) wv[r] = lds_pol(&W[own], pol_stream);
-                    if constexpr (kind_reads_x(KIND)) xv[r] = lds_pol(&X[own], pol_stream);
+                    if constexpr (kind_reads_w(KIND)) wv[r] = lds_pol(wrow[r], pol_stream);
+                    if constexpr (kind_reads_x(KIND)) xv[r] = lds_pol(wrow[r] + xdelta, pol_stream);
                 }
             };
             // own-row streams (W, X): loaded at the top of the column's step and consumed in
@@ -506,20 +514,19 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
             // (Handing a next-column register buffer over at the end of a step stalled on
             // the loads in flight: 23 % of the ncu samples.)
             constexpr int kPre = CFD_RING_PREFETCH;
-            auto prefetch_rows = [&](int c) {
+            auto prefetch_rows = [&](int ahead) {  // the own rows `ahead` columns ahead
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {
-                    const int64_t own = (rg0 + static_cast<int64_t>(G) * c + r) * pitch;
                     if constexpr (kind_reads_w(KIND))
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(&W[own]));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(wrow[r] + ahead * colstep));
                     if constexpr (kind_reads_x(KIND))
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(&X[own]));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(wrow[r] + xdelta + ahead * colstep));
                 }
             };
             if constexpr (kPre > 0) {
 #pragma unroll
                 for (int i = 1; i < kPre; ++i)
-                    if (xa + i < xb) prefetch_rows(xa + i);
+                    if (xa + i < xb) prefetch_rows(i);
             }
             for (int c = xa; c < xb; ++c) {
                 const int kz = c - xa;
@@ -528,9 +535,9 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
                 // static sites load their own rows now (consumed a whole step later); generic
                 // sites after their gathers, whose registers they would otherwise take
                 T wi[RS], xi[RS];
-                if (pat != 0) load_rows(c, wi, xi);
+                if (pat != 0) load_rows(wi, xi);
                 if constexpr (kPre > 0) {
-                    if (c + kPre < xb) prefetch_rows(c + kPre);
+                    if (c + kPre < xb) prefetch_rows(kPre);
                 }
                 const int need = min(c + 1, jhi - 1) - jlo;
                 while (kw <= need) {
@@ -606,14 +613,15 @@ __global__ void __launch_bounds__((kGroupRows / RS) * SY * US + 64, (US == 32 &&
 #pragma unroll
                     for (int r = 0; r < RS; ++r)
                         ui[r] = *reinterpret_cast<const T*>(b.own + (R0 + r) * RB);
-                    load_rows(c, wi, xi);
+                    load_rows(wi, xi);
                 }
 #pragma unroll
                 for (int r = 0; r < RS; ++r)
-                    step_epilogue<O, T, KIND, DMODE>(acc[r], ui[r], wi[r], xi[r], T{},
-                                                     (rg0 + static_cast<int64_t>(G) * c + r) * pitch, W, X,
+                    step_epilogue<O, T, KIND, DMODE>(acc[r], ui[r], wi[r], xi[r], T{}, 0, wrow[r], wrow[r] + xdelta,
                                                      static_cast<T*>(nullptr), p.beta, coeff, c1, c2,
                                                      acc_d, comp_d);
+#pragma unroll
+                for (int r = 0; r < RS; ++r) wrow[r] += colstep;
                 __syncwarp();
                 if (lane0) {
                     mbar_arrive(&empty_z[zslot]);
