@@ -118,9 +118,11 @@ enum { CHEBFD_OPT_GRAPHS = 1, CHEBFD_OPT_OVERLAP = 2, CHEBFD_OPT_KERNEL = 3,
  * rings by TMA bulk copies, consumer warps multiply straight from shared memory, so a site
  * block crosses L2 -> SM about once instead of once per referencing site.  Dot-free fused /
  * V_n-only steps; W and X bit-identical to the other step kernels.  1 (default): lattices
- * whose z-plane of the block reaches 2 x CHEBFD_OPT_BAND_BYTES (C4: 1 GB planes); 2: every
+ * whose z-plane of the block reaches 2 x CHEBFD_OPT_BAND_BYTES (C4: 1 GB planes), and from a
+ * quarter of that (8 MB) on where the grid is a dozen waves of CTAs (TI 64^3); 2: every
  * applicable launch; 0: off (the row-group / SELL kernels).
- * CHEBFD_OPT_RING_SEGX (x-columns per CTA, default 64), _NO / _NZ (ring depths, default
+ * CHEBFD_OPT_RING_SEGX (x-columns per CTA; default 0 = 64, halved down to 16 while the grid
+ * would be fewer than 24 waves of CTAs), _NO / _NZ (ring depths, default
  * 5 / 3), _ROWS (rows of a site per consumer thread: 4, 2 or 1; default 2 -- 4 / rows
  * consumer groups share a site's staged operands), _CONSTS (default 1: where every static
  * site of a pattern holds the same off-diagonal values -- the lattice models' hopping terms

@@ -707,12 +707,29 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     // L2-resident) 1.04 -> 1.15, where the SELL kernel stays.  2: wherever it applies
     // (planes of exactly 32 MB -- the C3 lattice at n_b = 32, the KPM block of its solve -- run
     // the ring kernel: filter 2.21 -> 1.97 ms per step, KPM of order 2000 2.95 -> 2.55 s)
-    if (ctx.ring == 1 &&
-        static_cast<size_t>(P) * units * 16 < 2 * static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 0)))
-        return false;
+    // x segment per CTA: 64 columns, halved down to 16 while the grid would be fewer than 24
+    // waves of resident CTAs -- medium lattices (TI 64^3, 96^2 x 32) ran 1024 - 1536 long CTAs,
+    // 3 - 10 waves with a ragged tail: TI 64^3 n_b = 64 1.00 -> 0.93 ms per filter step at 16
+    // columns, n_b = 32 0.63 -> 0.50; 8 columns lose again to the apron columns
+    const int64_t strips = ly / SY;
+    const double slots = static_cast<double>(ctx.num_sms) * (us == 32 ? 2 : 1);
+    auto waves = [&](int sx) { return static_cast<double>(strips * planes * ((lx + sx - 1) / sx)) / slots; };
+    int segx_auto = 64;
+    while (segx_auto > 16 && waves(segx_auto) < 24.0) segx_auto /= 2;
+    // Below 32 MB planes (L2-resident): with the short segments and the last session's lighter
+    // consumers the ring kernel also beats the SELL kernel from 8 MB planes on, given a dozen
+    // waves of CTAs (TI 64^3 n_b = 32: filter 0.52 -> 0.50 ms per step, fused step 0.74 -> 0.79
+    // of measured HBM; n_b = 64: 1.09 -> 0.93; TI 96^2 x 32 n_b = 32: 0.63 -> 0.70 of the
+    // schedule's bytes); smaller lattices (48^3, 32^3) stay on the SELL kernel
+    if (ctx.ring == 1) {
+        const size_t plane_b = static_cast<size_t>(P) * units * 16;
+        const size_t big = 2 * static_cast<size_t>(std::max<int64_t>(ctx.band_bytes, 0));
+        if (plane_b < big && (plane_b * 4 < big || waves(ctx.ring_segx > 0 ? ctx.ring_segx : segx_auto) < 12.0))
+            return false;
+    }
     const size_t rb = static_cast<size_t>(us) * 16;
     const size_t os = (SY + 2) * kGroupRows * rb, zs = SY * kGroupRows * rb + SY * kRingMaxVals * 16;
-    const int segx = static_cast<int>(std::min<int64_t>(lx, ctx.ring_segx > 0 ? ctx.ring_segx : 64));
+    const int segx = static_cast<int>(std::min<int64_t>(lx, ctx.ring_segx > 0 ? ctx.ring_segx : segx_auto));
     const size_t plan_b = static_cast<size_t>(SY) * segx * 32;
     int no = us == 64 ? 5 : 5, nz = 3;
     if (ctx.ring_no > 0) no = std::min(ctx.ring_no, kRingMaxDepth);
@@ -721,7 +738,6 @@ bool run_ring(Context& ctx, const StepArgs& s, cudaStream_t st, int units, int p
     const size_t smem = no * os + nz * zs + plan_b;
     if (smem > 220 * 1024) return false;
     // strips per band: the band's slice of the gathered operand within the band budget
-    const int64_t strips = ly / SY;
     int64_t spb = 1;
     for (int64_t d = 1; d <= strips; ++d)
         if (strips % d == 0 && static_cast<size_t>(d * SY * Ln) * units * 16 <=

@@ -20,7 +20,8 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
 CASES = {"c4": ((512, 512, 8), 64), "c3_256": ((128, 128, 64), 256), "c3_64": ((128, 128, 64), 64),
          "c3_32": ((128, 128, 64), 32), "c2": ((64, 64, 64), 32), "c2_64": ((64, 64, 64), 64),
          "c4_32": ((512, 512, 8), 32), "c4_128": ((512, 512, 4), 128),
-         "c4_256": ((512, 512, 2), 256)}
+         "c4_256": ((512, 512, 2), 256), "t32_64": ((32, 32, 32), 64), "t48_32": ((48, 48, 48), 32),
+         "t96_32": ((96, 96, 32), 32), "t96_64": ((96, 96, 32), 64), "t32_32": ((32, 32, 32), 32)}
 
 
 def main():
