@@ -25,11 +25,15 @@ def main():
     ap.add_argument("--nb", type=int, default=64)
     ap.add_argument("--lz", type=int, default=8)
     ap.add_argument("--compact", type=int, default=1)
+    ap.add_argument("--opt", action="append", default=[], help="context option name=value (repeatable)")
     args = ap.parse_args()
     t1 = None
     for P in (int(x) for x in args.ranks.split(",")):
         g = cf.VirtualGroup(P)
         g.set_option("compact_halo", args.compact)
+        for kv in args.opt:
+            k, v = kv.split("=")
+            g.set_option(k, int(v))
         spec = cf.LatticeSpec(512, 512, args.lz * P, disorder=0.5, seed=1)
         As = g.topological_insulator(spec)
         p = cf.make_filter((-0.3, 0.3), (-5.6, 5.6), args.deg, "lanczos2")
