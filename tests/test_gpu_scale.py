@@ -48,7 +48,11 @@ def test_c2_apply_filter_bitexact_vs_reference(ctx, ref_mt):
     X = cf.BlockVector(A, 32).randomize(7)  # the library's parallel stream of the same seed
     assert bits_equal(X.to_numpy(), x0)
     p = cf.make_filter((-0.28, 0.28), (-5.6, 5.6), 100, "lanczos2")
+    ring0 = ctx.ring_launches
     mom = cf.apply_filter(A, X, p, want_moments=True)
+    # steps 3 .. 100 -- the V_n-only steps with their doubling moment sums and the X-update
+    # steps -- ran on the site-ring kernel (default from 8 MB planes and a dozen waves of CTAs)
+    assert ctx.ring_launches - ring0 == 98
     xr, mr = ref_mt.apply_filter(m, x0, p.combined, p.alpha, p.beta, want_moments=True)
     assert bits_equal(X.to_numpy(), xr)
     assert np.max(np.abs(mom.m - mr)) <= 1e-12 * np.max(np.abs(mr[0]))
