@@ -58,7 +58,7 @@ WORKLOADS = {
     "c2": (64, 64, 64, 32, 100, False, "configs[1]"),
 }
 NCU_TRAFFIC = {  # committed ncu captures of the dominant kernel for a workload
-    "c4": "profiles/r02d_c4_ring_recur_step.json",
+    "c4": "profiles/r02e_c4_ring_recur_step.json",
     "c2": "profiles/r02_c2_recur_step.json",
 }
 
