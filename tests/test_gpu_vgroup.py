@@ -145,3 +145,29 @@ def test_band_order_keeps_the_bits(orc, world):
                 A.close()
     finally:
         g.close()
+
+
+def test_nccl_bootstrap_and_one_rank_distributed_context():
+    """The process-per-GPU entry (chebfd_ctx_create_dist, what `bench.py --gpus N` calls):
+    the library's own NCCL hands out a unique id on this box, and a one-rank distributed
+    context filters to the same bits as a plain context (no communicator, no halos)."""
+    uid = cf.Context.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    assert cf.Context.nccl_unique_id() != uid
+    spec = cf.LatticeSpec(5, 4, 6, disorder=0.5, seed=3)
+    p = cf.make_filter((-0.3, 0.3), (-5.6, 5.6), 17, "lanczos2")
+    out = []
+    for make in (lambda: cf.Context(0), lambda: cf.Context.distributed(0, 0, 1, uid)):
+        ctx = make()
+        try:
+            A = cf.SparseMatrix.topological_insulator(ctx, spec)
+            assert A.local_rows == A.dim()
+            X = cf.BlockVector(A, 8).randomize(5)
+            mom = cf.apply_filter(A, X, p, want_moments=True)
+            out.append((X.to_numpy(), np.asarray(mom.m)))
+        finally:
+            ctx.close()
+    assert bits_equal(out[0][0], out[1][0])
+    assert bits_equal(out[0][1], out[1][1])
+    with pytest.raises(cf.ChebfdError):
+        cf.Context.distributed(0, 2, 2, uid)  # rank outside the group
